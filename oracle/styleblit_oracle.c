@@ -1,0 +1,273 @@
+/*
+ * styleblit_oracle.c -- CPU ORACLE for StyleBlit (arXiv 1807.03249).
+ *
+ * TEST INFRASTRUCTURE ONLY: loaded by tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs.  Never linked into or called by the product
+ * (paper_1807_03249_b200/).  Shares no source with it.
+ *
+ * Plain C99, fp64 where the paper writes a real-valued formula, written in the paper's
+ * order and notation (Alg. 2; voting, lines 412-421).  No
+ * blocking, no tables, no reordering: it is meant to be checked against the paper by eye.
+ * Readings R1..R20 of ambiguous passages are listed in DESIGN.md.
+ *
+ * Pins (tests/test_oracle_*.py, -m "not gpu"): SURVEY App. A hash vectors, SPEC's
+ * worked SeedPoint/NearestSeed examples, closed-form NearestSeed on the zero-jitter
+ * grid, an independent numpy brute-force LUT, the identity / translation / t=0
+ * (Lit Sphere) closed forms, the seed-pixel property, the error bound, monotonicity
+ * in t, and a hand-computed vote.
+ */
+#include "styleblit_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+const char* or_version(void) { return "styleblit-oracle 1.0 (C99, fp64)"; }
+
+/* ------------------------------------------------------------------------------------ */
+/* R5: RandomJitterTable[b] realised as a stateless hash.  */
+/* ------------------------------------------------------------------------------------ */
+uint32_t or_lowbias32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    return x;
+}
+
+uint32_t or_cell_hash(int32_t bx, int32_t by, int32_t l, uint32_t seed) {
+    uint32_t c_l = or_lowbias32((uint32_t)l ^ or_lowbias32(seed));
+    return or_lowbias32((uint32_t)bx ^ or_lowbias32((uint32_t)by ^ c_l));
+}
+
+/* j in [0,1)^2: the low 16 bits of the hash give j_x, the high 16 bits give j_y. */
+void or_jitter(int32_t bx, int32_t by, int32_t l, uint32_t seed, int32_t zero_jitter,
+               double* jx, double* jy) {
+    if (zero_jitter) { *jx = 0.0; *jy = 0.0; return; }
+    uint32_t k = or_cell_hash(bx, by, l, seed);
+    *jx = (double)(k & 0xFFFFu) / 65536.0;
+    *jy = (double)(k >> 16) / 65536.0;
+}
+
+/* floor(p/h) toward -infinity (R6). */
+static int32_t floor_div(int32_t p, int32_t h) {
+    return (int32_t)floor((double)p / (double)h);
+}
+
+/* Alg. 2, SeedPoint:
+ *   b = floor(p/h);  j = RandomJitterTable[b];  return floor(h * (b + j)).      */
+void or_seed_point_j(int32_t px, int32_t py, int32_t h, double jx, double jy,
+                     int32_t* sx, int32_t* sy) {
+    int32_t bx = floor_div(px, h), by = floor_div(py, h);
+    *sx = (int32_t)floor((double)h * ((double)bx + jx));
+    *sy = (int32_t)floor((double)h * ((double)by + jy));
+}
+
+void or_seed_point(int32_t px, int32_t py, int32_t l, uint32_t seed, int32_t zero_jitter,
+                   int32_t* sx, int32_t* sy) {
+    int32_t h = 1 << l;
+    int32_t bx = floor_div(px, h), by = floor_div(py, h);
+    double jx, jy;
+    or_jitter(bx, by, l, seed, zero_jitter, &jx, &jy);
+    or_seed_point_j(px, py, h, jx, jy, sx, sy);
+}
+
+/* Alg. 2, NearestSeed.  x outer, y inner, keep the first strictly
+ * smaller d = ||s - p|| (Euclidean, in fp64; exact ordering for integer offsets, R1, R7). */
+void or_nearest_seed(int32_t px, int32_t py, int32_t l, uint32_t seed, int32_t zero_jitter,
+                     int32_t* qx, int32_t* qy) {
+    int32_t h = 1 << l;
+    double d_star = INFINITY;
+    int32_t best_x = 0, best_y = 0;
+    for (int32_t x = -1; x <= 1; ++x) {
+        for (int32_t y = -1; y <= 1; ++y) {
+            int32_t sx, sy;
+            or_seed_point(px + h * x, py + h * y, l, seed, zero_jitter, &sx, &sy);
+            double dx = (double)sx - (double)px, dy = (double)sy - (double)py;
+            double d = sqrt(dx * dx + dy * dy);
+            if (d < d_star) { best_x = sx; best_y = sy; d_star = d; }
+        }
+    }
+    *qx = best_x;
+    *qy = best_y;
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Guide look-up table ("simple look-up table", Alg. 2).       */
+/* ------------------------------------------------------------------------------------ */
+uint32_t or_lut_entry(const uint8_t* gs, int32_t ws, int32_t hs, int32_t g0, int32_t g1) {
+    /* u* = argmin_u ||(g0,g1) - G_S[u].(c0,c1)||, scanning u in row-major order and keeping
+     * the first strict minimum (R10).  The squared norm has the same argmin.           */
+    int64_t best = -1;
+    uint32_t best_u = 0;
+    for (int32_t y = 0; y < hs; ++y) {
+        for (int32_t x = 0; x < ws; ++x) {
+            const uint8_t* g = gs + 4 * ((int64_t)y * ws + x);
+            int64_t d0 = (int64_t)g0 - g[0], d1 = (int64_t)g1 - g[1];
+            int64_t d = d0 * d0 + d1 * d1;
+            if (best < 0 || d < best) { best = d; best_u = (uint32_t)x | ((uint32_t)y << 16); }
+        }
+    }
+    return best_u;
+}
+
+typedef struct {
+    const uint8_t* gs; int32_t ws, hs; uint32_t* lut; int32_t k_begin, k_end;
+} lut_job;
+
+static void* lut_worker(void* arg) {
+    lut_job* j = (lut_job*)arg;
+    for (int32_t k = j->k_begin; k < j->k_end; ++k)
+        j->lut[k] = or_lut_entry(j->gs, j->ws, j->hs, k & 0xFF, k >> 8);
+    return NULL;
+}
+
+void or_build_lut(const uint8_t* gs, int32_t ws, int32_t hs, uint32_t* lut, int32_t nthreads) {
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    lut_job jobs[256];
+    for (int32_t i = 0; i < nthreads; ++i) {
+        jobs[i].gs = gs; jobs[i].ws = ws; jobs[i].hs = hs; jobs[i].lut = lut;
+        jobs[i].k_begin = (int32_t)((int64_t)65536 * i / nthreads);
+        jobs[i].k_end = (int32_t)((int64_t)65536 * (i + 1) / nthreads);
+    }
+    if (nthreads == 1) { lut_worker(&jobs[0]); return; }
+    for (int32_t i = 0; i < nthreads; ++i) pthread_create(&th[i], NULL, lut_worker, &jobs[i]);
+    for (int32_t i = 0; i < nthreads; ++i) pthread_join(th[i], NULL);
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Alg. 2, ParallelStyleBlit.                                         */
+/* ------------------------------------------------------------------------------------ */
+static int32_t clampi(int32_t v, int32_t lo, int32_t hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+/* LUT key of a guide value: channels 0 and 1 (R11). */
+static uint32_t lut_at(const uint32_t* lut, const uint8_t* g) { return lut[(uint32_t)g[0] | ((uint32_t)g[1] << 8)]; }
+
+void or_stylize_pixel(const or_params* prm, const uint8_t* gs, int32_t ws, int32_t hs,
+                      const uint32_t* lut, const uint8_t* gt, int32_t wt, int32_t ht,
+                      int32_t px, int32_t py, uint32_t* coord, uint8_t* level) {
+    const uint8_t* gt_p = gt + 4 * ((int64_t)py * wt + px);
+    for (int32_t l = prm->L; l >= 1; --l) {                               /* line 380 */
+        int32_t qx, qy;
+        or_nearest_seed(px, py, l, prm->seed, prm->zero_jitter, &qx, &qy); /* line 382 */
+        qx = clampi(qx, 0, wt - 1);                                        /* R8 */
+        qy = clampi(qy, 0, ht - 1);
+        uint32_t u = lut_at(lut, gt + 4 * ((int64_t)qy * wt + qx));        /* line 383 */
+        int32_t ux = (int32_t)(u & 0xFFFFu), uy = (int32_t)(u >> 16);
+        int32_t sx = ux + (px - qx), sy = uy + (py - qy);                  /* u* + (p - q_l) */
+        if (sx < 0 || sx >= ws || sy < 0 || sy >= hs) continue;           /* R9 */
+        const uint8_t* gs_s = gs + 4 * ((int64_t)sy * ws + sx);
+        double e2 = 0.0;                                                   /* line 384, R1 */
+        for (int32_t c = 0; c < prm->C; ++c) {
+            double d = (double)gt_p[c] - (double)gs_s[c];
+            e2 += d * d;
+        }
+        double e = sqrt(e2);
+        if (e < prm->t) {                                                  /* line 385, R3 */
+            *coord = (uint32_t)sx | ((uint32_t)sy << 16);                  /* line 387 */
+            *level = (uint8_t)l;
+            return;                                                        /* line 388 */
+        }
+    }
+    *coord = lut_at(lut, gt_p);                                            /* R12 */
+    *level = 0;
+}
+
+typedef struct {
+    const or_params* prm; const uint8_t* cs; const uint8_t* gs; int32_t ws, hs;
+    const uint32_t* lut; const uint8_t* gt; int32_t wt, ht;
+    uint8_t* ct; uint32_t* coords; uint8_t* level; int32_t y_begin, y_end;
+} sty_job;
+
+static void* sty_worker(void* arg) {
+    sty_job* j = (sty_job*)arg;
+    for (int32_t py = j->y_begin; py < j->y_end; ++py) {
+        for (int32_t px = 0; px < j->wt; ++px) {
+            int64_t i = (int64_t)py * j->wt + px;
+            uint32_t c; uint8_t lv;
+            or_stylize_pixel(j->prm, j->gs, j->ws, j->hs, j->lut, j->gt, j->wt, j->ht, px, py, &c, &lv);
+            if (j->coords) j->coords[i] = c;
+            if (j->level) j->level[i] = lv;
+            if (j->ct) {                                                   /* C_T[p] = C_S[s] */
+                int64_t si = (int64_t)(c >> 16) * j->ws + (c & 0xFFFFu);
+                memcpy(j->ct + 4 * i, j->cs + 4 * si, 4);
+            }
+        }
+    }
+    return NULL;
+}
+
+void or_stylize(const or_params* prm, const uint8_t* cs, const uint8_t* gs, int32_t ws, int32_t hs,
+                const uint32_t* lut, const uint8_t* gt, int32_t wt, int32_t ht,
+                uint8_t* ct, uint32_t* coords, uint8_t* level, int32_t nthreads) {
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    sty_job jobs[256];
+    for (int32_t i = 0; i < nthreads; ++i) {
+        sty_job j = {prm, cs, gs, ws, hs, lut, gt, wt, ht, ct, coords, level,
+                     (int32_t)((int64_t)ht * i / nthreads), (int32_t)((int64_t)ht * (i + 1) / nthreads)};
+        jobs[i] = j;
+    }
+    if (nthreads == 1) { sty_worker(&jobs[0]); return; }
+    for (int32_t i = 0; i < nthreads; ++i) pthread_create(&th[i], NULL, sty_worker, &jobs[i]);
+    for (int32_t i = 0; i < nthreads; ++i) pthread_join(th[i], NULL);
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Voting (R13, R14).                                                  */
+/* C_T[p] = average over target pixels q with |q - p|_inf <= r (clipped to the target)   */
+/* of C_S[src(q) + (p - q)], skipping positions outside the source; per channel          */
+/* floor((sum + floor(n/2)) / n).                                                        */
+/* ------------------------------------------------------------------------------------ */
+typedef struct {
+    const uint32_t* coords; int32_t wt, ht; const uint8_t* cs; int32_t ws, hs, r;
+    uint8_t* ct; int32_t y_begin, y_end;
+} vote_job;
+
+static void* vote_worker(void* arg) {
+    vote_job* j = (vote_job*)arg;
+    for (int32_t py = j->y_begin; py < j->y_end; ++py) {
+        for (int32_t px = 0; px < j->wt; ++px) {
+            uint64_t sum[4] = {0, 0, 0, 0};
+            uint64_t n = 0;
+            for (int32_t qy = py - j->r; qy <= py + j->r; ++qy) {
+                for (int32_t qx = px - j->r; qx <= px + j->r; ++qx) {
+                    if (qx < 0 || qx >= j->wt || qy < 0 || qy >= j->ht) continue;
+                    uint32_t src = j->coords[(int64_t)qy * j->wt + qx];
+                    int32_t sx = (int32_t)(src & 0xFFFFu) + (px - qx);
+                    int32_t sy = (int32_t)(src >> 16) + (py - qy);
+                    if (sx < 0 || sx >= j->ws || sy < 0 || sy >= j->hs) continue;
+                    const uint8_t* c = j->cs + 4 * ((int64_t)sy * j->ws + sx);
+                    for (int32_t ch = 0; ch < 4; ++ch) sum[ch] += c[ch];
+                    n += 1;
+                }
+            }
+            uint8_t* out = j->ct + 4 * ((int64_t)py * j->wt + px);
+            if (n == 0) { memset(out, 0, 4); continue; }   /* unreachable for valid coords */
+            for (int32_t ch = 0; ch < 4; ++ch)
+                out[ch] = (uint8_t)((sum[ch] + n / 2) / n);   /* n >= 1: q = p always counts */
+        }
+    }
+    return NULL;
+}
+
+void or_vote(const uint32_t* coords, int32_t wt, int32_t ht, const uint8_t* cs, int32_t ws,
+             int32_t hs, int32_t r, uint8_t* ct, int32_t nthreads) {
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    vote_job jobs[256];
+    for (int32_t i = 0; i < nthreads; ++i) {
+        vote_job j = {coords, wt, ht, cs, ws, hs, r, ct,
+                      (int32_t)((int64_t)ht * i / nthreads), (int32_t)((int64_t)ht * (i + 1) / nthreads)};
+        jobs[i] = j;
+    }
+    if (nthreads == 1) { vote_worker(&jobs[0]); return; }
+    for (int32_t i = 0; i < nthreads; ++i) pthread_create(&th[i], NULL, vote_worker, &jobs[i]);
+    for (int32_t i = 0; i < nthreads; ++i) pthread_join(th[i], NULL);
+}
