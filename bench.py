@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""StyleBlit (arXiv 1807.03249) hot-path benchmark on B200.
+
+One STEP = one pass of the whole hot path over one batch of synthetic 4K frames per GPU:
+  sb_build_lut (the exemplar's guide LUT)
+  + sb_stylize_batch (Alg. 2 for every pixel of every frame, per-frame jitter seeds,
+    PAPER.md:337-433; coordinates out)
+  + sb_vote (the voting blend; colours out).
+Workload (BASELINE.json configs[4] = config 5, per GPU): B frames of 3840x2160 heightfield
+normals (seed 5, per-frame phase), 512x512 sphere exemplar, L=5, t=10, C=3, r=2.
+Frames are sharded by rank (weak scaling: every GPU stylizes its own B frames, no data-path
+collective).  Inputs are > L2 (B*33 MB of G_T per step), so no L2 flush is needed.
+
+`value` = whole-job stylized megapixels/s (device-resident inputs, CUDA-event timing, max over
+ranks).  `e2e` = the same through sb_stylize_batch_host with pinned host buffers (host->device
+copies of G_T and device->host copies of C_T inside the timed region).
+
+`--impl reference` runs the CPU oracle (oracle/, the reference arm of this tier) on the same
+config: each step = one 4K frame (stylize + vote) on all host cores, LUT built before timing.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WT, HT = 3840, 2160
+CFG_ID = 5
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--frames", type=int, default=64, help="4K frames per GPU per step")
+    ap.add_argument("--blend-radius", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--json-out", default=None)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons DURING the timed region."""
+
+    def __init__(self, index: int, period_s: float = 0.02):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.max_mhz = None
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ----------------------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1807_03249_b200 as sb
+    import synth
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    cfg = synth.CONFIGS[CFG_ID]
+    B, r = args.frames, args.blend_radius
+    # exemplar replicated on every GPU; frames of this rank: global indices rank*B .. rank*B+B-1
+    cs, gs = [t.to(dev) for t in synth.exemplar(cfg, device=dev)]
+    base = synth.heightfield_normals(WT, HT, seed=5, frame=0, device=dev)
+    gt = torch.empty(B, HT, WT, 4, dtype=torch.uint8, device=dev)
+    n_distinct = min(B, 8)  # G_T content barely matters for speed; 8 distinct phases, cycled
+    for i in range(n_distinct):
+        gt[i] = synth.heightfield_normals(WT, HT, seed=5, frame=rank * B + i, device=dev)
+    for i in range(n_distinct, B):
+        gt[i] = gt[i % n_distinct]
+    del base
+    seeds = [(cfg["seed"] + rank * B + i) & 0xFFFFFFFF for i in range(B)]
+    coords = torch.empty(B, HT, WT, dtype=torch.int32, device=dev)
+    ct = torch.empty(B, HT, WT, 4, dtype=torch.uint8, device=dev)
+    lut = torch.empty(65536, dtype=torch.int32, device=dev)
+    lut_ws = torch.empty(65536 * 4, dtype=torch.uint8, device=dev)
+    prm = sb.Params(threshold=cfg["t"], levels=cfg["L"], blend_radius=0, guide_channels=cfg["C"],
+                    seed=cfg["seed"], flags=sb.SB_NO_COLOR)
+    stream = torch.cuda.current_stream(dev)
+
+    ev = {k: [] for k in ("lut", "stylize", "vote")}
+    launches = [0]
+
+    def step(record: bool):
+        es = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if record else None
+        if record:
+            es[0].record(stream)
+        sb.build_lut(gs, lut, lut_ws)
+        n_l = sb.launch_count()
+        if record:
+            es[1].record(stream)
+        sb.stylize_batch(prm, cs, gs, lut, gt, frame_seeds=seeds, ct=None, coords=coords, want_level=False)
+        n_s = sb.launch_count()
+        if record:
+            es[2].record(stream)
+        sb.vote(coords, cs, r, ct=ct)
+        n_v = sb.launch_count()
+        if record:
+            es[3].record(stream)
+            ev["lut"].append((es[0], es[1]))
+            ev["stylize"].append((es[1], es[2]))
+            ev["vote"].append((es[2], es[3]))
+            launches[0] += n_l + n_s + n_v
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for _ in range(args.steps):
+            step(True)
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_step = ms / args.steps
+    px_step = B * WT * HT
+    value = world * px_step / (ms_step * 1e-3) / 1e6  # MP/s, whole job
+
+    kt = {k: statistics.mean(a.elapsed_time(b) for a, b in v) for k, v in ev.items()}
+    hbm, hbm_src = peaks()
+    # algorithmic bytes per launch: stylize reads G_T, writes coords;
+    # vote reads coords, writes C_T: 8 B per pixel each.
+    alg = {"stylize": 8 * px_step, "vote": 8 * px_step, "lut": gs.numel() + 65536 * 4}
+    dom = max(("stylize", "vote"), key=lambda k: kt[k])
+    ach = alg[dom] / (kt[dom] * 1e-3) / 1e9
+    kernels = {k: {"ms_per_launch": round(kt[k], 4), "share": round(kt[k] / ms_step, 4),
+                   "GBps_alg": round(alg[k] / (kt[k] * 1e-3) / 1e9, 1)} for k in kt}
+
+    # ---- e2e through the host-buffer ABI call (pinned host memory, copies inside timing)
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        Be = min(B, 16)
+        gt_h = gt[:Be].cpu().pin_memory()
+        ct_h = torch.empty_like(gt_h).pin_memory()
+        prm_e = sb.Params(threshold=cfg["t"], levels=cfg["L"], blend_radius=r, guide_channels=cfg["C"],
+                          seed=cfg["seed"])
+        ws_e = sb.host_workspace(WT, HT, r, 2, device=dev)
+
+        def e2e_step():
+            sb.build_lut(gs, lut, lut_ws)
+            sb.stylize_batch_host(prm_e, cs, gs, lut, gt_h, ct_h, frame_seeds=seeds[:Be], workspace=ws_e, depth=2)
+
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = a.elapsed_time(b) / args.e2e_steps
+        if world > 1:
+            tt = torch.tensor([ems], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        e2e = {"value": round(world * Be * WT * HT / (ems * 1e-3) / 1e6, 1), "unit": "MP/s",
+               "h2d_bytes_per_step": Be * WT * HT * 4, "d2h_bytes_per_step": Be * WT * HT * 4,
+               "frames_per_step": Be, "ms_per_step": round(ems, 3),
+               "api": "sb_stylize_batch_host (pinned host G_T in, pinned host C_T out, 2-deep copy/compute pipeline)"}
+
+    # ---- parity spot check of this run's outputs (sampled pixels of frame 0 vs oracle) is in tests/.
+    out = {
+        "metric": "stylized megapixels/s (4K UHD frames/s) per B200 and 8-GPU; % HBM roofline",
+        "value": round(value, 1),
+        "unit": "MP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8",
+        "data": "synthetic (seeded heightfield-normal 4K frames, sphere-normal exemplar, painted style)",
+        "config": {"workload": f"cfg5: {B} x 4K UHD (3840x2160) frames per GPU, 512x512 exemplar, L={cfg['L']}, "
+                               f"t={cfg['t']}, C={cfg['C']}, blend r={r}; step = LUT build + stylize + vote",
+                   "frames_per_gpu": B, "global_frames": B * world, "levels": cfg["L"], "threshold": cfg["t"],
+                   "blend_radius": r, "parallelism": f"frame-sharded x{world} (no data-path collective)",
+                   "l2": "inputs larger than L2 (G_T %.2f GB per GPU per step); no flush" % (4 * px_step / 1e9)},
+        "fps_4k": round(value * 1e6 / (WT * HT), 1),
+        "kernels": kernels,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(ach / hbm, 4), "traffic": None, "peak_source": hbm_src,
+                     "alg_bytes_per_launch": alg[dom], "alg_bytes_per_px": 8},
+        "gpu_launches": launches[0],
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    return out, rank, world
+
+
+# ----------------------------------------------------------------------------------- oracle
+def oracle_sample(n_frames: int, r: int, nthreads: int):
+    """The oracle (as it stands) on n 4K frames of the same workload: LUT, stylize, vote."""
+    import numpy as np
+
+    import oracle
+    import synth
+
+    cfg = synth.CONFIGS[CFG_ID]
+    cs, gs = [t.numpy() for t in synth.exemplar(cfg)]
+    frames = [synth.heightfield_normals(WT, HT, seed=5, frame=i).numpy() for i in range(n_frames)]
+    t0 = time.perf_counter()
+    lut = oracle.build_lut(gs, nthreads=nthreads)
+    t1 = time.perf_counter()
+    for i, f in enumerate(frames):
+        prm = oracle.Params(t=cfg["t"], L=cfg["L"], C=cfg["C"], seed=(cfg["seed"] + i) & 0xFFFFFFFF)
+        _, coords, _ = oracle.stylize(prm, cs, gs, lut, f, nthreads=nthreads)
+        if r > 0:
+            oracle.vote(coords, cs, r, nthreads=nthreads)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1, lut, cs, gs, frames, np
+
+
+def cpu_baseline(args):
+    n = 4
+    nth = os.cpu_count() or 1
+    t_lut, t_frames, *_ = oracle_sample(n, args.blend_radius, nth)
+    tot = t_lut + t_frames
+    return {"value": round(n * WT * HT / tot / 1e6, 3), "unit": "MP/s", "cores": nth, "kind": "oracle",
+            "sample": f"LUT build + {n} 4K frames (stylize + vote r={args.blend_radius}) of the cfg5 workload on "
+                      f"{nth} host threads; {tot:.1f} s (LUT {t_lut:.1f} s)"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return None, rank, world
+    import oracle
+    import synth
+
+    cfg = synth.CONFIGS[CFG_ID]
+    nth = os.cpu_count() or 1
+    cs, gs = [t.numpy() for t in synth.exemplar(cfg)]
+    lut = oracle.build_lut(gs, nthreads=nth)
+    frames = [synth.heightfield_normals(WT, HT, seed=5, frame=i).numpy() for i in range(2)]
+    r = args.blend_radius
+
+    def step(i):
+        prm = oracle.Params(t=cfg["t"], L=cfg["L"], C=cfg["C"], seed=(cfg["seed"] + i) & 0xFFFFFFFF)
+        _, coords, _ = oracle.stylize(prm, cs, gs, lut, frames[i % 2], nthreads=nth)
+        if r > 0:
+            oracle.vote(coords, cs, r, nthreads=nth)
+
+    for i in range(args.warmup):
+        step(i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step(i)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = round(WT * HT / dt / 1e6, 3)
+    out = {
+        "impl": "reference",
+        "metric": "stylized megapixels/s (4K UHD frames/s) per B200 and 8-GPU; % HBM roofline",
+        "value": v, "unit": "MP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u8", "data": "synthetic",
+        "config": {"workload": f"cfg5: 4K UHD frames, 512x512 exemplar, L={cfg['L']}, t={cfg['t']}, C={cfg['C']}, "
+                               f"blend r={r}; reference step = 1 frame on the CPU oracle (LUT built before timing)"},
+        "cpu_baseline": {"value": v, "unit": "MP/s", "cores": nth, "kind": "oracle",
+                         "sample": f"1 4K frame per step (stylize + vote r={r}), {nth} host threads"},
+        "e2e": {"value": v, "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return out, rank, world
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        out, rank, world = run_reference(args)
+    else:
+        out, rank, world = run_ours(args)
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(args)
+    if rank == 0 and out is not None:
+        line = json.dumps(out)
+        print(line, flush=True)
+        if args.json_out:
+            with open(args.json_out, "w") as f:
+                f.write(line + "\n")
+    if args.impl == "ours" and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

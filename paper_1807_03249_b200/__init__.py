@@ -1,0 +1,193 @@
+"""StyleBlit (arXiv 1807.03249) hot path on B200: a thin Python binding of include/styleblit.h.
+
+The names match the C ABI (``sb_build_lut`` -> :func:`build_lut`, ``sb_stylize`` ->
+:func:`stylize`, ``sb_stylize_batch`` -> :func:`stylize_batch`,
+``sb_stylize_batch_host`` -> :func:`stylize_batch_host`).  This module only marshals
+arguments: every step of the method runs in the sm_100a kernels of ``libstyleblit.so``.
+PyTorch provides device memory and the current CUDA stream.  There is no CPU fallback: the
+functions raise if the library is missing or a tensor is not on a CUDA device.
+
+Tensors: images are ``uint8 [H, W, 4]`` (batches ``[N, H, W, 4]``), the LUT is ``int32
+[65536]`` (reinterpreted as uint32), coordinates are ``int32 [H, W]`` holding ``x | y << 16``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import SB_JITTER_ZERO, SB_NO_COLOR, StyleBlitError, check, lib
+
+__all__ = [
+    "Params", "build_lut", "stylize", "stylize_batch", "vote", "stylize_batch_host", "launch_count",
+    "version", "SB_JITTER_ZERO", "SB_NO_COLOR", "StyleBlitError",
+]
+
+
+@dataclass
+class Params:
+    """sb_params: the paper's t and L plus blend radius, channels, jitter seed."""
+
+    threshold: float
+    levels: int
+    blend_radius: int = 0
+    guide_channels: int = 3
+    seed: int = 0x5EED
+    flags: int = 0
+    row_begin: int = 0
+    row_end: int = 0
+
+    def c(self) -> _lib.SbParams:
+        return _lib.SbParams(float(self.threshold), int(self.levels), int(self.blend_radius),
+                             int(self.guide_channels), int(self.seed) & 0xFFFFFFFF, int(self.flags),
+                             int(self.row_begin), int(self.row_end))
+
+
+def _dev(t: torch.Tensor, name: str, dtype: torch.dtype, ndim: tuple[int, ...]) -> int:
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if t.dim() not in ndim:
+        raise ValueError(f"{name} must have {ndim} dims, got {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t.data_ptr()
+
+
+def _img_wh(t: torch.Tensor, name: str) -> tuple[int, int]:
+    if t.shape[-1] != 4:
+        raise ValueError(f"{name} must have 4 bytes per pixel, got shape {tuple(t.shape)}")
+    return int(t.shape[-2]), int(t.shape[-3])
+
+
+def _stream(stream) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def build_lut(gs: torch.Tensor, lut: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+              stream=None) -> torch.Tensor:
+    """sb_build_lut: the exact 256x256 guide look-up table of G_S."""
+    _dev(gs, "gs", torch.uint8, (3,))
+    ws, hs = _img_wh(gs, "gs")
+    if lut is None:
+        lut = torch.empty(65536, dtype=torch.int32, device=gs.device)
+    _dev(lut, "lut", torch.int32, (1,))
+    if workspace is None:
+        workspace = torch.empty(lib().sb_lut_workspace_bytes(), dtype=torch.uint8, device=gs.device)
+    check(lib().sb_build_lut(gs.data_ptr(), ws, hs, lut.data_ptr(), workspace.data_ptr(), _stream(stream)))
+    return lut
+
+
+def _outputs(prm: Params, shape_px: tuple[int, ...], device, ct, coords, level, want_level: bool):
+    no_color = bool(prm.flags & SB_NO_COLOR)
+    if ct is None and not no_color:
+        ct = torch.empty(*shape_px, 4, dtype=torch.uint8, device=device)
+    if coords is None:
+        coords = torch.empty(*shape_px, dtype=torch.int32, device=device)
+    if level is None and want_level:
+        level = torch.empty(*shape_px, dtype=torch.uint8, device=device)
+    return ct, coords, level
+
+
+def stylize(prm: Params, cs: torch.Tensor, gs: torch.Tensor, lut: torch.Tensor, gt: torch.Tensor,
+            ct: torch.Tensor | None = None, coords: torch.Tensor | None = None, level: torch.Tensor | None = None,
+            want_level: bool = True, stream=None):
+    """sb_stylize: Alg. 2 for every pixel of G_T (+ voting when prm.blend_radius > 0).
+    Returns (ct, coords, level)."""
+    return stylize_batch(prm, cs, gs, lut, gt.unsqueeze(0), None,
+                         None if ct is None else ct.unsqueeze(0),
+                         None if coords is None else coords.unsqueeze(0),
+                         None if level is None else level.unsqueeze(0), want_level, stream, _squeeze=True)
+
+
+def stylize_batch(prm: Params, cs: torch.Tensor, gs: torch.Tensor, lut: torch.Tensor, gt: torch.Tensor,
+                  frame_seeds=None, ct: torch.Tensor | None = None, coords: torch.Tensor | None = None,
+                  level: torch.Tensor | None = None, want_level: bool = True, stream=None, _squeeze: bool = False):
+    """sb_stylize_batch over gt [N, H, W, 4]; frame i jittered with frame_seeds[i]
+    (default prm.seed + i).  Returns (ct, coords, level)."""
+    _dev(cs, "cs", torch.uint8, (3,))
+    _dev(gs, "gs", torch.uint8, (3,))
+    _dev(lut, "lut", torch.int32, (1,))
+    _dev(gt, "gt", torch.uint8, (4,))
+    ws, hs = _img_wh(gs, "gs")
+    if _img_wh(cs, "cs") != (ws, hs):
+        raise ValueError("cs and gs must have the same size")
+    n = int(gt.shape[0])
+    wt, ht = _img_wh(gt, "gt")
+    ct, coords, level = _outputs(prm, (n, ht, wt), gt.device, ct, coords, level, want_level)
+    ptr = lambda t, name, dt, nd: 0 if t is None else _dev(t, name, dt, nd)  # noqa: E731
+    seeds = None
+    if frame_seeds is not None:
+        seeds = (C.c_uint32 * n)(*[int(s) & 0xFFFFFFFF for s in frame_seeds])
+    p = prm.c()
+    check(lib().sb_stylize_batch(C.byref(p), n, seeds, cs.data_ptr(), gs.data_ptr(), ws, hs, lut.data_ptr(),
+                                 gt.data_ptr(), wt, ht, ptr(ct, "ct", torch.uint8, (4,)),
+                                 ptr(coords, "coords", torch.int32, (3,)), ptr(level, "level", torch.uint8, (3,)),
+                                 _stream(stream)))
+    if _squeeze:
+        sq = lambda t: None if t is None else t[0]  # noqa: E731
+        return sq(ct), sq(coords), sq(level)
+    return ct, coords, level
+
+
+def vote(coords: torch.Tensor, cs: torch.Tensor, r: int, ct: torch.Tensor | None = None,
+         row_begin: int = 0, row_end: int = 0, stream=None) -> torch.Tensor:
+    """sb_vote: C_T from a coordinate field.  coords [H,W] or [N,H,W] int32."""
+    squeeze = coords.dim() == 2
+    co = coords.unsqueeze(0) if squeeze else coords
+    _dev(co, "coords", torch.int32, (3,))
+    _dev(cs, "cs", torch.uint8, (3,))
+    n, ht, wt = (int(v) for v in co.shape)
+    ws, hs = _img_wh(cs, "cs")
+    if ct is None:
+        ct = torch.empty(n, ht, wt, 4, dtype=torch.uint8, device=co.device)
+    elif squeeze:
+        ct = ct.unsqueeze(0)
+    _dev(ct, "ct", torch.uint8, (4,))
+    check(lib().sb_vote(co.data_ptr(), n, wt, ht, cs.data_ptr(), ws, hs, int(r), ct.data_ptr(), int(row_begin),
+                        int(row_end), _stream(stream)))
+    return ct[0] if squeeze else ct
+
+
+def host_workspace(wt: int, ht: int, blend_radius: int = 0, depth: int = 2, device="cuda") -> torch.Tensor:
+    return torch.empty(lib().sb_host_workspace_bytes(wt, ht, blend_radius, depth), dtype=torch.uint8, device=device)
+
+
+def stylize_batch_host(prm: Params, cs: torch.Tensor, gs: torch.Tensor, lut: torch.Tensor, gt_host: torch.Tensor,
+                       ct_host: torch.Tensor, coords_host: torch.Tensor | None = None, frame_seeds=None,
+                       workspace: torch.Tensor | None = None, depth: int = 2, stream=None):
+    """sb_stylize_batch_host: HOST gt [N,H,W,4] in, HOST ct [N,H,W,4] out (pinned memory for
+    full copy bandwidth); copies and compute overlap inside the library.  Blocks until done."""
+    for t, name in ((gt_host, "gt_host"), (ct_host, "ct_host")):
+        if t.is_cuda or t.dtype != torch.uint8 or not t.is_contiguous() or t.dim() != 4:
+            raise ValueError(f"{name} must be a contiguous host uint8 [N,H,W,4] tensor")
+    n = int(gt_host.shape[0])
+    wt, ht = _img_wh(gt_host, "gt_host")
+    ws, hs = _img_wh(gs, "gs")
+    if workspace is None:
+        workspace = host_workspace(wt, ht, prm.blend_radius, depth, device=cs.device)
+    seeds = None
+    if frame_seeds is not None:
+        seeds = (C.c_uint32 * n)(*[int(s) & 0xFFFFFFFF for s in frame_seeds])
+    p = prm.c()
+    check(lib().sb_stylize_batch_host(C.byref(p), n, seeds, _dev(cs, "cs", torch.uint8, (3,)),
+                                      _dev(gs, "gs", torch.uint8, (3,)), ws, hs, _dev(lut, "lut", torch.int32, (1,)),
+                                      gt_host.data_ptr(), wt, ht, ct_host.data_ptr(),
+                                      0 if coords_host is None else coords_host.data_ptr(),
+                                      workspace.data_ptr(), workspace.numel(), depth, _stream(stream)))
+    return ct_host
+
+
+def launch_count() -> int:
+    """Kernels launched by the last ABI call on this thread."""
+    return int(lib().sb_last_launch_count())
+
+
+def version() -> str:
+    return lib().sb_version().decode()

@@ -1,0 +1,324 @@
+// api.cu -- the C ABI of include/styleblit.h: argument validation, T2 conversion, launches,
+// and the host-streaming batch pipeline.  No compute happens on the host: every step of the
+// method runs in the kernels of lut_build.cu, stylize.cu / stylize_naive.cu and vote.cu.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "../../include/styleblit.h"
+#include "sb_kernels.cuh"
+
+namespace {
+
+thread_local char g_err[512] = "";
+thread_local int g_launches = 0;
+
+sb_status fail(sb_status s, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return s;
+}
+
+sb_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(SB_ECUDA, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+constexpr int kMaxDim = 32767;
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+sb_status check_dims(const char* name, int32_t w, int32_t h) {
+    if (w < 1 || w > kMaxDim || h < 1 || h > kMaxDim)
+        return fail(SB_EINVAL, "%s: dimensions %dx%d outside [1,%d]", name, w, h, kMaxDim);
+    return SB_OK;
+}
+
+// Which stylize kernel: the tiled kernel needs wt % 4 == 0 (uint4 pixel groups per row);
+// SB_KERNEL=naive selects the one-thread-per-pixel kernel (for A/B measurement).
+bool use_naive(int32_t wt) {
+    static const int forced = [] {
+        const char* e = getenv("SB_KERNEL");
+        return (e && strcmp(e, "naive") == 0) ? 1 : 0;
+    }();
+    return forced || (wt % 4) != 0;
+}
+
+struct Prepared {
+    sb::StylizeArgs s;
+    sb::VoteArgs v;
+    bool vote;
+};
+
+sb_status validate(const sb_params* prm, int32_t n_frames, const uint8_t* cs, const uint8_t* gs, int32_t ws,
+                   int32_t hs, const uint32_t* lut, const uint8_t* gt, int32_t wt, int32_t ht, uint8_t* ct,
+                   uint32_t* coords, bool device_outputs, Prepared* out) {
+    if (!prm) return fail(SB_EINVAL, "prm is NULL");
+    if (n_frames < 0) return fail(SB_EINVAL, "n_frames=%d < 0", n_frames);
+    sb_status s;
+    if ((s = check_dims("source (ws,hs)", ws, hs)) != SB_OK) return s;
+    if ((s = check_dims("target (wt,ht)", wt, ht)) != SB_OK) return s;
+    const float t = prm->threshold;
+    if (!std::isfinite(t) || t < 0.f) return fail(SB_EINVAL, "threshold t=%g must be finite and >= 0", (double)t);
+    if (prm->levels < 1 || prm->levels > SB_MAX_LEVELS)
+        return fail(SB_EINVAL, "levels L=%d outside [1,%d]", prm->levels, SB_MAX_LEVELS);
+    if (prm->blend_radius < 0 || prm->blend_radius > SB_MAX_RADIUS)
+        return fail(SB_EINVAL, "blend_radius r=%d outside [0,%d]", prm->blend_radius, SB_MAX_RADIUS);
+    if (prm->guide_channels < 2 || prm->guide_channels > 4)
+        return fail(SB_EINVAL, "guide_channels C=%d not in {2,3,4}", prm->guide_channels);
+    if (prm->flags & ~(SB_JITTER_ZERO | SB_NO_COLOR)) return fail(SB_EINVAL, "flags 0x%x has unknown bits", prm->flags);
+    int rb = prm->row_begin, re = prm->row_end;
+    if (rb == 0 && re == 0) re = ht;
+    if (rb < 0 || re > ht || rb >= re)
+        return fail(SB_EINVAL, "rows [row_begin=%d,row_end=%d) not a non-empty range inside [0,%d)", prm->row_begin,
+                    prm->row_end, ht);
+    if (!cs) return fail(SB_EINVAL, "cs (style exemplar C_S) is NULL");
+    if (!gs) return fail(SB_EINVAL, "gs (source guide G_S) is NULL");
+    if (!lut) return fail(SB_EINVAL, "lut is NULL");
+    if (!gt) return fail(SB_EINVAL, "gt (target guide G_T) is NULL");
+    const bool no_color = (prm->flags & SB_NO_COLOR) != 0;
+    const int r = prm->blend_radius;
+    if (!no_color && !ct) return fail(SB_EINVAL, "ct is NULL (pass SB_NO_COLOR to skip colours)");
+    if (r > 0 && !no_color && !coords) return fail(SB_EINVAL, "coords is NULL but blend_radius=%d needs it", r);
+    if (device_outputs) {
+        if (!aligned16(cs) || !aligned16(gs) || !aligned16(gt) || (ct && !aligned16(ct)) ||
+            (coords && !aligned16(coords)) || !aligned16(lut))
+            return fail(SB_EINVAL, "image/LUT base pointers must be 16-byte aligned");
+    }
+
+    Prepared& p = *out;
+    memset(&p, 0, sizeof(p));
+    sb::StylizeArgs& a = p.s;
+    a.cs = cs; a.gs = gs; a.ws = ws; a.hs = hs; a.lut = lut; a.gt = gt; a.wt = wt; a.ht = ht;
+    a.L = prm->levels;
+    const double t2 = std::ceil((double)t * (double)t);  // exact: t is a float (reading R2)
+    a.T2 = t2 >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)t2;
+    a.cmask = prm->guide_channels == 4 ? 0xFFFFFFFFu : (prm->guide_channels == 3 ? 0x00FFFFFFu : 0x0000FFFFu);
+    a.zero_jitter = (prm->flags & SB_JITTER_ZERO) ? 1 : 0;
+    a.seed_base = prm->seed;
+    a.coords = coords;
+    p.vote = (r > 0) && !no_color;
+    // rows computed by the stylize kernel: the output strip plus the vote's coords halo
+    a.row_begin = p.vote ? (rb - r < 0 ? 0 : rb - r) : rb;
+    a.row_end = p.vote ? (re + r > ht ? ht : re + r) : re;
+    a.ct = (no_color || p.vote) ? nullptr : ct;
+    if (p.vote) {
+        sb::VoteArgs& v = p.v;
+        v.coords = coords; v.cs = cs; v.ws = ws; v.hs = hs; v.wt = wt; v.ht = ht; v.r = r; v.ct = ct;
+        v.row_begin = rb; v.row_end = re;
+    }
+    return SB_OK;
+}
+
+// Launch stylize (+vote) for n frames starting at frame offset f0 of the given buffers.
+sb_status launch_frames(Prepared& p, int n_frames, const uint32_t* frame_seeds, uint32_t seed_base_f0,
+                        uint8_t* level, cudaStream_t st) {
+    const int64_t fpx = (int64_t)p.s.wt * p.s.ht;
+    for (int f0 = 0; f0 < n_frames; f0 += sb::kSeedsPerLaunch) {
+        const int nf = (n_frames - f0) < sb::kSeedsPerLaunch ? (n_frames - f0) : sb::kSeedsPerLaunch;
+        sb::StylizeArgs a = p.s;
+        a.gt = p.s.gt + 4 * fpx * f0;
+        a.ct = p.s.ct ? p.s.ct + 4 * fpx * f0 : nullptr;
+        a.coords = p.s.coords ? p.s.coords + fpx * f0 : nullptr;
+        a.level = level ? level + fpx * f0 : nullptr;
+        a.has_seeds = frame_seeds ? 1 : 0;
+        a.seed_base = seed_base_f0 + (uint32_t)f0;
+        if (frame_seeds) memcpy(a.seeds, frame_seeds + f0, sizeof(uint32_t) * nf);
+        cudaError_t e = use_naive(a.wt) ? sb::launch_stylize_naive(a, nf, st, &g_launches)
+                                        : sb::launch_stylize_tiled(a, nf, st, &g_launches);
+        if (e != cudaSuccess) return cuda_fail(e, "stylize launch");
+        if (p.vote) {
+            sb::VoteArgs v = p.v;
+            v.coords = a.coords;
+            v.ct = p.v.ct + 4 * fpx * f0;
+            e = sb::launch_vote(v, nf, st, &g_launches);
+            if (e != cudaSuccess) return cuda_fail(e, "vote launch");
+        }
+    }
+    return SB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t sb_lut_workspace_bytes(void) { return 65536 * sizeof(uint32_t); }
+
+sb_status sb_build_lut(const uint8_t* gs, int32_t ws, int32_t hs, uint32_t* lut, void* workspace, void* stream) {
+    g_launches = 0;
+    sb_status s;
+    if (!gs) return fail(SB_EINVAL, "gs (source guide G_S) is NULL");
+    if (!lut) return fail(SB_EINVAL, "lut is NULL");
+    if (!workspace) return fail(SB_EINVAL, "workspace is NULL (need sb_lut_workspace_bytes() bytes)");
+    if ((s = check_dims("source (ws,hs)", ws, hs)) != SB_OK) return s;
+    if (!aligned16(gs) || !aligned16(workspace) || !aligned16(lut))
+        return fail(SB_EINVAL, "gs/lut/workspace must be 16-byte aligned");
+    cudaError_t e = sb::launch_build_lut(gs, ws, hs, lut, workspace, (cudaStream_t)stream, &g_launches);
+    if (e != cudaSuccess) return cuda_fail(e, "sb_build_lut launch");
+    return SB_OK;
+}
+
+sb_status sb_stylize(const sb_params* prm, const uint8_t* cs, const uint8_t* gs, int32_t ws, int32_t hs,
+                     const uint32_t* lut, const uint8_t* gt, int32_t wt, int32_t ht, uint8_t* ct, uint32_t* coords,
+                     uint8_t* level, void* stream) {
+    return sb_stylize_batch(prm, 1, nullptr, cs, gs, ws, hs, lut, gt, wt, ht, ct, coords, level, stream);
+}
+
+sb_status sb_stylize_batch(const sb_params* prm, int32_t n_frames, const uint32_t* frame_seeds, const uint8_t* cs,
+                           const uint8_t* gs, int32_t ws, int32_t hs, const uint32_t* lut, const uint8_t* gt,
+                           int32_t wt, int32_t ht, uint8_t* ct, uint32_t* coords, uint8_t* level, void* stream) {
+    g_launches = 0;
+    Prepared p;
+    sb_status s = validate(prm, n_frames, cs, gs, ws, hs, lut, gt, wt, ht, ct, coords, true, &p);
+    if (s != SB_OK) return s;
+    if (level && !aligned16(level)) return fail(SB_EINVAL, "level must be 16-byte aligned");
+    if (n_frames == 0) return SB_OK;
+    return launch_frames(p, n_frames, frame_seeds, prm->seed, level, (cudaStream_t)stream);
+}
+
+sb_status sb_vote(const uint32_t* coords, int32_t n_frames, int32_t wt, int32_t ht, const uint8_t* cs, int32_t ws,
+                  int32_t hs, int32_t r, uint8_t* ct, int32_t row_begin, int32_t row_end, void* stream) {
+    g_launches = 0;
+    sb_status s;
+    if (!coords) return fail(SB_EINVAL, "coords is NULL");
+    if (!cs) return fail(SB_EINVAL, "cs (style exemplar C_S) is NULL");
+    if (!ct) return fail(SB_EINVAL, "ct is NULL");
+    if (n_frames < 0) return fail(SB_EINVAL, "n_frames=%d < 0", n_frames);
+    if ((s = check_dims("source (ws,hs)", ws, hs)) != SB_OK) return s;
+    if ((s = check_dims("target (wt,ht)", wt, ht)) != SB_OK) return s;
+    if (r < 0 || r > SB_MAX_RADIUS) return fail(SB_EINVAL, "r=%d outside [0,%d]", r, SB_MAX_RADIUS);
+    if (row_begin == 0 && row_end == 0) row_end = ht;
+    if (row_begin < 0 || row_end > ht || row_begin >= row_end)
+        return fail(SB_EINVAL, "rows [row_begin=%d,row_end=%d) not a non-empty range inside [0,%d)", row_begin, row_end,
+                    ht);
+    if (!aligned16(coords) || !aligned16(cs) || !aligned16(ct))
+        return fail(SB_EINVAL, "coords/cs/ct must be 16-byte aligned");
+    if (wt % 4 != 0) return fail(SB_EUNSUPPORTED, "sb_vote needs wt %% 4 == 0 (got %d); use sb_stylize", wt);
+    const int64_t fpx = (int64_t)wt * ht;
+    for (int f0 = 0; f0 < n_frames; f0 += 65535) {
+        const int nf = (n_frames - f0) < 65535 ? (n_frames - f0) : 65535;
+        sb::VoteArgs v;
+        v.coords = coords + fpx * f0; v.cs = cs; v.ws = ws; v.hs = hs; v.wt = wt; v.ht = ht; v.r = r;
+        v.ct = ct + 4 * fpx * f0; v.row_begin = row_begin; v.row_end = row_end;
+        cudaError_t e = sb::launch_vote(v, nf, (cudaStream_t)stream, &g_launches);
+        if (e != cudaSuccess) return cuda_fail(e, "vote launch");
+    }
+    return SB_OK;
+}
+
+// One slot of the host pipeline: G_T, C_T and coords of one frame, each 256-byte aligned.
+static size_t host_seg_bytes(int32_t wt, int32_t ht) { return (((size_t)wt * (size_t)ht * 4) + 255) & ~(size_t)255; }
+
+size_t sb_host_workspace_bytes(int32_t wt, int32_t ht, int32_t blend_radius, int32_t depth) {
+    if (wt < 1 || ht < 1 || depth < 1) return 0;
+    (void)blend_radius;
+    return 3 * host_seg_bytes(wt, ht) * (size_t)depth;
+}
+
+sb_status sb_stylize_batch_host(const sb_params* prm, int32_t n_frames, const uint32_t* frame_seeds,
+                                const uint8_t* cs, const uint8_t* gs, int32_t ws, int32_t hs, const uint32_t* lut,
+                                const uint8_t* gt_host, int32_t wt, int32_t ht, uint8_t* ct_host,
+                                uint32_t* coords_host, void* workspace, size_t workspace_bytes, int32_t depth,
+                                void* stream) {
+    g_launches = 0;
+    if (depth < 1 || depth > 8) return fail(SB_EINVAL, "depth=%d outside [1,8]", depth);
+    if (!workspace) return fail(SB_EINVAL, "workspace is NULL");
+    if (!gt_host) return fail(SB_EINVAL, "gt_host is NULL");
+    if (!ct_host && !(prm && (prm->flags & SB_NO_COLOR))) return fail(SB_EINVAL, "ct_host is NULL");
+    if (workspace_bytes < sb_host_workspace_bytes(wt, ht, prm ? prm->blend_radius : 0, depth))
+        return fail(SB_EINVAL, "workspace_bytes=%zu < sb_host_workspace_bytes()=%zu", workspace_bytes,
+                    sb_host_workspace_bytes(wt, ht, prm ? prm->blend_radius : 0, depth));
+    if (!aligned16(workspace)) return fail(SB_EINVAL, "workspace must be 16-byte aligned");
+    // Validate against slot 0 (device pointers) so the per-frame launches cannot fail validation.
+    if (wt < 1 || ht < 1) return fail(SB_EINVAL, "target (wt,ht): dimensions %dx%d", wt, ht);
+    const size_t fpx = (size_t)wt * (size_t)ht;
+    const size_t seg = host_seg_bytes(wt, ht);
+    auto slot_ptr = [&](int k, int part) { return static_cast<uint8_t*>(workspace) + ((size_t)k * 3 + part) * seg; };
+    Prepared p;
+    sb_status s = validate(prm, 1, cs, gs, ws, hs, lut, slot_ptr(0, 0), wt, ht, slot_ptr(0, 1),
+                           reinterpret_cast<uint32_t*>(slot_ptr(0, 2)), true, &p);
+    if (s != SB_OK) return s;
+    if (prm->row_begin != 0 || prm->row_end != 0) return fail(SB_EUNSUPPORTED, "host batches are whole frames");
+    if (n_frames == 0) return SB_OK;
+
+    cudaStream_t user = (cudaStream_t)stream;
+    cudaStream_t sH2D, sCmp, sD2H;
+    cudaError_t e;
+    if ((e = cudaStreamCreateWithFlags(&sH2D, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
+    cudaStreamCreateWithFlags(&sCmp, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&sD2H, cudaStreamNonBlocking);
+    cudaEvent_t start, *inReady = new cudaEvent_t[depth], *cmpDone = new cudaEvent_t[depth],
+                       *outDone = new cudaEvent_t[depth];
+    cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+    for (int k = 0; k < depth; ++k) {
+        cudaEventCreateWithFlags(&inReady[k], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&cmpDone[k], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&outDone[k], cudaEventDisableTiming);
+    }
+    // everything is ordered after the work already queued on the caller's stream
+    cudaEventRecord(start, user);
+    cudaStreamWaitEvent(sH2D, start, 0);
+    cudaStreamWaitEvent(sCmp, start, 0);
+    int total_launches = 0;
+    sb_status st = SB_OK;
+    for (int i = 0; i < n_frames && st == SB_OK; ++i) {
+        const int k = i % depth;
+        uint8_t* dgt = slot_ptr(k, 0);
+        uint8_t* dct = slot_ptr(k, 1);
+        uint32_t* dco = reinterpret_cast<uint32_t*>(slot_ptr(k, 2));
+        if (i >= depth) cudaStreamWaitEvent(sH2D, outDone[k], 0);  // slot free again
+        e = cudaMemcpyAsync(dgt, gt_host + 4 * fpx * (size_t)i, 4 * fpx, cudaMemcpyHostToDevice, sH2D);
+        if (e != cudaSuccess) { st = cuda_fail(e, "H2D copy"); break; }
+        cudaEventRecord(inReady[k], sH2D);
+        cudaStreamWaitEvent(sCmp, inReady[k], 0);
+        Prepared pf = p;
+        pf.s.gt = dgt;
+        pf.s.ct = pf.s.ct ? dct : nullptr;
+        pf.s.coords = dco;
+        if (pf.vote) { pf.v.coords = dco; pf.v.ct = dct; }
+        const uint32_t seed_i = frame_seeds ? frame_seeds[i] : prm->seed + (uint32_t)i;
+        st = launch_frames(pf, 1, nullptr, seed_i, nullptr, sCmp);
+        total_launches += g_launches;
+        g_launches = 0;
+        if (st != SB_OK) break;
+        cudaEventRecord(cmpDone[k], sCmp);
+        cudaStreamWaitEvent(sD2H, cmpDone[k], 0);
+        if (ct_host) {
+            e = cudaMemcpyAsync(ct_host + 4 * fpx * (size_t)i, dct, 4 * fpx, cudaMemcpyDeviceToHost, sD2H);
+            if (e != cudaSuccess) { st = cuda_fail(e, "D2H copy"); break; }
+        }
+        if (coords_host) {
+            e = cudaMemcpyAsync(coords_host + fpx * (size_t)i, dco, 4 * fpx, cudaMemcpyDeviceToHost, sD2H);
+            if (e != cudaSuccess) { st = cuda_fail(e, "D2H copy"); break; }
+        }
+        cudaEventRecord(outDone[k], sD2H);
+    }
+    e = cudaStreamSynchronize(sD2H);
+    cudaError_t e2 = cudaStreamSynchronize(sCmp);
+    cudaStreamSynchronize(sH2D);
+    if (st == SB_OK && e != cudaSuccess) st = cuda_fail(e, "pipeline sync");
+    if (st == SB_OK && e2 != cudaSuccess) st = cuda_fail(e2, "pipeline sync");
+    for (int k = 0; k < depth; ++k) {
+        cudaEventDestroy(inReady[k]);
+        cudaEventDestroy(cmpDone[k]);
+        cudaEventDestroy(outDone[k]);
+    }
+    delete[] inReady;
+    delete[] cmpDone;
+    delete[] outDone;
+    cudaEventDestroy(start);
+    cudaStreamDestroy(sH2D);
+    cudaStreamDestroy(sCmp);
+    cudaStreamDestroy(sD2H);
+    g_launches = total_launches;
+    return st;
+}
+
+int32_t sb_last_launch_count(void) { return g_launches; }
+const char* sb_last_error(void) { return g_err; }
+const char* sb_version(void) { return "styleblit-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

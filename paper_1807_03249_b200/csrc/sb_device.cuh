@@ -1,0 +1,77 @@
+// sb_device.cuh -- device helpers shared by the StyleBlit kernels (sm_100a).
+//
+// Integer-only formulations of the paper's operations; see DESIGN.md "Kernels".
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sb {
+
+// RandomJitterTable realised by the stateless hash of reading R5.
+__device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    return x;
+}
+
+// Seed of cell b at level l (SeedPoint): h*b + floor(h*j) with the 16-bit
+// jitter j of R5, i.e. the top l bits of each 16-bit half of the hash.  c_l is the
+// per-(frame, level) salt lowbias32(l ^ lowbias32(seed)).
+__device__ __forceinline__ void cell_seed(int bx, int by, int l, uint32_t c_l, bool zero_jitter,
+                                          int& sx, int& sy) {
+    const uint32_t k = lowbias32((uint32_t)bx ^ lowbias32((uint32_t)by ^ c_l));
+    const int jx = zero_jitter ? 0 : (int)((k & 0xFFFFu) >> (16 - l));
+    const int jy = zero_jitter ? 0 : (int)(k >> (32 - l));
+    sx = bx * (1 << l) + jx;
+    sy = by * (1 << l) + jy;
+}
+
+__host__ __device__ __forceinline__ uint32_t level_salt(uint32_t seed, int l) {
+#ifdef __CUDA_ARCH__
+    return lowbias32((uint32_t)l ^ lowbias32(seed));
+#else
+    auto h = [](uint32_t x) {
+        x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16; return x;
+    };
+    return h((uint32_t)l ^ h(seed));
+#endif
+}
+
+// Squared guide error over the channels selected by cmask (0x0000FFFF, 0x00FFFFFF or
+// 0xFFFFFFFF): VABSDIFF4 + LOP3 + IDP.4A.
+__device__ __forceinline__ uint32_t guide_d2(uint32_t a, uint32_t b, uint32_t cmask) {
+    const uint32_t d = __vabsdiffu4(a, b) & cmask;
+    return __dp4a(d, d, 0u);
+}
+
+__device__ __forceinline__ uint32_t pack_xy(int x, int y) { return (uint32_t)x | ((uint32_t)y << 16); }
+
+// Streaming (evict-first) 128-bit global stores for outputs written once.
+__device__ __forceinline__ void st_cs_u4(void* p, uint4 v) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void st_cs_u32(void* p, uint32_t v) {
+    asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// L2 policy for data streamed once (G_T in, outputs out): evict first, so the exemplar,
+// G_S and the LUT (re-read by every tile) keep their L2 residency.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// Streaming 128-bit load of G_T (read once per pixel).
+__device__ __forceinline__ uint4 ld_stream_u4(const void* p, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
+}  // namespace sb

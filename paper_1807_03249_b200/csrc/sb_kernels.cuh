@@ -1,0 +1,48 @@
+// sb_kernels.cuh -- kernel argument blocks and launchers of libstyleblit (sm_100a).
+#pragma once
+#include "sb_device.cuh"
+
+namespace sb {
+
+constexpr int kSeedsPerLaunch = 512;  // frames per launch (per-frame seeds travel as params)
+
+struct StylizeArgs {
+    const uint8_t* cs;
+    const uint8_t* gs;
+    int ws, hs;
+    const uint32_t* lut;
+    const uint8_t* gt;  // frame 0 of this launch
+    int wt, ht;
+    uint8_t* ct;        // NULL: no colour output (SB_NO_COLOR or vote follows)
+    uint32_t* coords;   // may be NULL
+    uint8_t* level;     // may be NULL
+    int L;
+    uint32_t T2;        // accept iff D < T2 (= ceil(t*t), saturated)
+    uint32_t cmask;     // guide channel byte mask for D
+    int zero_jitter;
+    int row_begin, row_end;  // rows computed
+    uint32_t seed_base;
+    int has_seeds;
+    uint32_t seeds[kSeedsPerLaunch];
+    __device__ __forceinline__ uint32_t frame_seed(int f) const {
+        return has_seeds ? seeds[f] : seed_base + (uint32_t)f;
+    }
+};
+
+struct VoteArgs {
+    const uint32_t* coords;  // frame 0 of this launch
+    const uint8_t* cs;
+    int ws, hs;
+    int wt, ht;
+    int r;
+    uint8_t* ct;
+    int row_begin, row_end;  // rows written
+};
+
+cudaError_t launch_build_lut(const uint8_t* gs, int ws, int hs, uint32_t* lut, void* workspace,
+                             cudaStream_t st, int* launches);
+cudaError_t launch_stylize_naive(const StylizeArgs& a, int n_frames, cudaStream_t st, int* launches);
+cudaError_t launch_stylize_tiled(const StylizeArgs& a, int n_frames, cudaStream_t st, int* launches);
+cudaError_t launch_vote(const VoteArgs& a, int n_frames, cudaStream_t st, int* launches);
+
+}  // namespace sb

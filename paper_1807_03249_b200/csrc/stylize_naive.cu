@@ -1,0 +1,66 @@
+// stylize_naive.cu -- one thread per target pixel, Alg. 2 written straight.
+//
+// Kept as the simple baseline kernel (selected with SB_KERNEL=naive) against which the
+// tiled kernel in stylize.cu is measured; both must agree bit for bit with the oracle.
+#include "sb_kernels.cuh"
+
+namespace sb {
+
+__global__ void __launch_bounds__(256) stylize_naive_kernel(StylizeArgs a) {
+    const int frame = blockIdx.y;
+    const int64_t npx = (int64_t)(a.row_end - a.row_begin) * a.wt;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= npx) return;
+    const int py = a.row_begin + (int)(i / a.wt);
+    const int px = (int)(i % a.wt);
+    const int64_t fpx = (int64_t)a.wt * a.ht;
+    const uint32_t* gt = reinterpret_cast<const uint32_t*>(a.gt) + fpx * frame;
+    const uint32_t* gs = reinterpret_cast<const uint32_t*>(a.gs);
+    const uint32_t seed = a.frame_seed(frame);
+    const bool zj = a.zero_jitter;
+    const uint32_t gp = __ldg(gt + (int64_t)py * a.wt + px);
+
+    uint32_t coord = 0;
+    int level = 0;
+    for (int l = a.L; l >= 1; --l) {
+        const uint32_t c_l = level_salt(seed, l);
+        const int bx = px >> l, by = py >> l;
+        uint32_t best = 0xFFFFFFFFu;
+        int qx = 0, qy = 0;
+        // NearestSeed: x outer, y inner, first strict minimum
+        for (int x = -1; x <= 1; ++x)
+            for (int y = -1; y <= 1; ++y) {
+                int sx, sy;
+                cell_seed(bx + x, by + y, l, c_l, zj, sx, sy);
+                const int dx = sx - px, dy = sy - py;
+                const uint32_t d = (uint32_t)(dx * dx + dy * dy);
+                if (d < best) { best = d; qx = sx; qy = sy; }
+            }
+        qx = min(max(qx, 0), a.wt - 1);  // R8
+        qy = min(max(qy, 0), a.ht - 1);
+        const uint32_t u = __ldg(a.lut + (__ldg(gt + (int64_t)qy * a.wt + qx) & 0xFFFFu));
+        const int sx = (int)(u & 0xFFFFu) + (px - qx);
+        const int sy = (int)(u >> 16) + (py - qy);
+        if ((unsigned)sx >= (unsigned)a.ws || (unsigned)sy >= (unsigned)a.hs) continue;  // R9
+        const uint32_t d2 = guide_d2(gp, __ldg(gs + (int64_t)sy * a.ws + sx), a.cmask);
+        if (d2 < a.T2) { coord = pack_xy(sx, sy); level = l; break; }
+    }
+    if (level == 0) coord = __ldg(a.lut + (gp & 0xFFFFu));  // R12
+    const int64_t o = fpx * frame + (int64_t)py * a.wt + px;
+    if (a.coords) a.coords[o] = coord;
+    if (a.level) a.level[o] = (uint8_t)level;
+    if (a.ct) {
+        const uint32_t c = __ldg(reinterpret_cast<const uint32_t*>(a.cs) + (int64_t)(coord >> 16) * a.ws + (coord & 0xFFFFu));
+        reinterpret_cast<uint32_t*>(a.ct)[o] = c;
+    }
+}
+
+cudaError_t launch_stylize_naive(const StylizeArgs& a, int n_frames, cudaStream_t st, int* launches) {
+    const int64_t npx = (int64_t)(a.row_end - a.row_begin) * a.wt;
+    dim3 grid((unsigned)((npx + 255) / 256), (unsigned)n_frames);
+    stylize_naive_kernel<<<grid, 256, 0, st>>>(a);
+    *launches += 1;
+    return cudaPeekAtLastError();
+}
+
+}  // namespace sb

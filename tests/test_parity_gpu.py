@@ -1,0 +1,283 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bar (BASELINE.json north_star): LUT, source-coordinate maps and levels bit-exact; blit colours
+bit-exact; voted colours within max-abs 1/255 -- the integer vote is in fact checked
+bit-exact here.  Inputs are the seeded synthetic configs of synth/ plus edge cases.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1807_03249_b200 as sb
+import synth
+
+pytestmark = pytest.mark.gpu
+NTH = min(16, os.cpu_count() or 1)
+DEV = "cuda"
+
+
+def u32(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint32)
+
+
+_lut_cache = {}
+
+
+def oracle_lut(gs: np.ndarray) -> np.ndarray:
+    key = (gs.shape, gs.tobytes().__hash__())
+    if key not in _lut_cache:
+        _lut_cache[key] = oracle.build_lut(gs, nthreads=NTH)
+    return _lut_cache[key]
+
+
+def run_both(prm: sb.Params, cs, gs, gt, want_vote=True):
+    """Run GPU and oracle on identical bytes; return dict of arrays."""
+    csd, gsd, gtd = cs.to(DEV), gs.to(DEV), gt.to(DEV)
+    lut_d = sb.build_lut(gsd)
+    ct, coords, level = sb.stylize(prm, csd, gsd, lut_d, gtd)
+    torch.cuda.synchronize()
+    csn, gsn, gtn = cs.numpy(), gs.numpy(), gt.numpy()
+    lut = oracle_lut(gsn)
+    oprm = oracle.Params(t=prm.threshold, L=prm.levels, C=prm.guide_channels, seed=prm.seed,
+                         zero_jitter=bool(prm.flags & sb.SB_JITTER_ZERO))
+    oct_, oco, olv = oracle.stylize(oprm, csn, gsn, lut, gtn, nthreads=NTH)
+    if prm.blend_radius > 0:
+        oct_ = oracle.vote(oco, csn, prm.blend_radius, nthreads=NTH)
+    return dict(lut=(u32(lut_d), lut), coords=(u32(coords), oco), level=(level.cpu().numpy(), olv),
+                ct=(ct.cpu().numpy(), oct_))
+
+
+def assert_exact(res, name):
+    g, o = res[name]
+    if not (g == o).all():
+        bad = np.argwhere(g != o)
+        raise AssertionError(f"{name}: {len(bad)} mismatches, first at {bad[:5].tolist()}: gpu {g[tuple(bad[0])]} "
+                             f"oracle {o[tuple(bad[0])]}")
+
+
+# ------------------------------------------------------------------ LUT
+@pytest.mark.parametrize("kind", ["sphere64", "sphere512", "uv256", "uv1024", "const", "rand_small", "rand_few"])
+def test_lut_all_keys(kind):
+    rng = np.random.RandomState(7)
+    if kind == "sphere64":
+        gs = synth.sphere_normal(64, 64)
+    elif kind == "sphere512":
+        gs = synth.sphere_normal(512, 512)
+    elif kind == "uv256":
+        gs = synth.uv_identity(256, 256)
+    elif kind == "uv1024":
+        gs = synth.uv_identity(1024, 1024)
+    elif kind == "const":
+        gs = torch.full((17, 9, 4), 200, dtype=torch.uint8)
+    elif kind == "rand_small":
+        gs = torch.from_numpy(rng.randint(0, 256, (5, 7, 4)).astype(np.uint8))
+    else:  # few distinct values, many ties
+        gs = torch.from_numpy((rng.randint(0, 3, (40, 33, 4)) * 100).astype(np.uint8))
+    gsn = gs.numpy()
+    got = u32(sb.build_lut(gs.to(DEV)))
+    if gsn.shape[0] * gsn.shape[1] <= 512 * 512:
+        want = oracle_lut(gsn)
+        assert (got == want).all(), np.argwhere(got != want)[:5]
+    else:  # 1024^2: sampled keys, each by the oracle's definition
+        for k in np.random.RandomState(1).randint(0, 65536, 300).tolist() + [0, 65535]:
+            assert got[k] == oracle.lut_entry(gsn, k & 0xFF, k >> 8), k
+
+
+# ------------------------------------------------------------------ configs 1-4 full frames
+@pytest.mark.parametrize("cid", [1, 2, 3, 4])
+def test_config_parity(cid):
+    cfg = synth.CONFIGS[cid]
+    cs, gs = synth.exemplar(cfg)
+    gt = synth.target(cid)
+    for r in sorted({0, cfg["r"]}):
+        prm = sb.Params(threshold=cfg["t"], levels=cfg["L"], blend_radius=r, guide_channels=cfg["C"], seed=cfg["seed"])
+        res = run_both(prm, cs, gs, gt)
+        for n in ("lut", "coords", "level", "ct"):
+            assert_exact(res, n)
+        lv = res["level"][1]
+        assert (lv == cfg["L"]).mean() > 0.3 and (lv < cfg["L"]).any()  # the hierarchy is exercised
+
+
+# ------------------------------------------------------------------ edge cases
+def _rand_case(wt, ht, ws, hs, seed, C=3, vmax=256):
+    rng = np.random.RandomState(seed)
+    gs = synth.sphere_normal(ws, hs)
+    cs = torch.from_numpy(rng.randint(0, 256, (hs, ws, 4)).astype(np.uint8))
+    gt = synth.heightfield_normals(wt, ht, seed=seed)
+    return cs, gs, gt
+
+
+@pytest.mark.parametrize("wt,ht", [(1, 1), (3, 5), (4, 1), (130, 17), (127, 33), (132, 16), (256, 48), (8, 300)])
+@pytest.mark.parametrize("L", [1, 2, 5])
+def test_ragged_sizes(wt, ht, L):
+    """Tile-ragged widths/heights, widths not divisible by 4 (one-thread-per-pixel kernel),
+    single-pixel images, L = 1 (no top-level group pass)."""
+    cs, gs, gt = _rand_case(wt, ht, 48, 40, seed=wt * 1000 + ht)
+    for r in (0, 2):
+        prm = sb.Params(threshold=14.0, levels=L, blend_radius=r, guide_channels=3, seed=99)
+        res = run_both(prm, cs, gs, gt)
+        for n in ("coords", "level", "ct"):
+            assert_exact(res, n)
+
+
+@pytest.mark.parametrize("t", [0.0, 0.5, 1.0, 6.0, 1000.0])
+@pytest.mark.parametrize("C", [2, 3, 4])
+def test_thresholds_and_channels(t, C):
+    cs, gs, gt = _rand_case(200, 72, 64, 64, seed=5)
+    gt = gt.clone()
+    gt[..., 3] = torch.from_numpy(np.random.RandomState(3).randint(0, 4, gt.shape[:2]).astype(np.uint8))
+    prm = sb.Params(threshold=t, levels=4, blend_radius=0, guide_channels=C, seed=7)
+    res = run_both(prm, cs, gs, gt)
+    for n in ("coords", "level", "ct"):
+        assert_exact(res, n)
+    if t == 0.0:
+        assert (res["level"][0] == 0).all()
+
+
+@pytest.mark.parametrize("L", [3, 8, 12])
+def test_zero_jitter_and_deep_hierarchies(L):
+    cs, gs, gt = _rand_case(256, 96, 64, 64, seed=11)
+    for flags in (0, sb.SB_JITTER_ZERO):
+        prm = sb.Params(threshold=9.0, levels=L, blend_radius=1, guide_channels=3, seed=3, flags=flags)
+        res = run_both(prm, cs, gs, gt)
+        for n in ("coords", "level", "ct"):
+            assert_exact(res, n)
+
+
+@pytest.mark.parametrize("r", [1, 3, 7])
+def test_vote_radii(r):
+    cfg = synth.CONFIGS[2]
+    cs, gs = synth.exemplar(cfg)
+    gt = synth.render_objects(256, 160, seed=2)
+    prm = sb.Params(threshold=cfg["t"], levels=5, blend_radius=r, guide_channels=3, seed=cfg["seed"])
+    res = run_both(prm, cs, gs, gt)
+    assert_exact(res, "coords")
+    g, o = res["ct"]
+    assert np.abs(g.astype(int) - o.astype(int)).max() <= 1  # north-star tolerance (1/255)
+    assert_exact(res, "ct")  # the integer vote is in fact exact
+
+
+def test_identity_transfer_gpu():
+    """G_T = G_S injective -> coords = p, level = L, C_T = C_S."""
+    g = np.zeros((64, 64, 4), np.uint8)
+    g[..., 0] = (np.arange(64) * 4)[None, :]
+    g[..., 1] = (np.arange(64) * 4)[:, None]
+    gs = torch.from_numpy(g)
+    cs = synth.painted_style(64, 64)
+    prm = sb.Params(threshold=0.5, levels=5, blend_radius=2, guide_channels=3)
+    ct, coords, lv = sb.stylize(prm, cs.to(DEV), gs.to(DEV), sb.build_lut(gs.to(DEV)), gs.to(DEV))
+    yy, xx = np.mgrid[0:64, 0:64]
+    assert (u32(coords) == (xx | (yy << 16))).all()
+    assert (lv.cpu().numpy() == 5).all()
+    assert (ct.cpu().numpy() == cs.numpy()).all()
+
+
+# ------------------------------------------------------------------ batch, strips, determinism
+def test_batch_equals_single_frames():
+    cfg = synth.CONFIGS[2]
+    cs, gs = [t.to(DEV) for t in synth.exemplar(cfg)]
+    lut = sb.build_lut(gs)
+    frames = torch.stack([synth.heightfield_normals(320, 200, seed=9, frame=i) for i in range(5)]).to(DEV)
+    for r in (0, 2):
+        prm = sb.Params(threshold=10.0, levels=5, blend_radius=r, guide_channels=3, seed=100)
+        seeds = [100, 7, 7, 0xFFFFFFFF, 12345]
+        bct, bco, blv = sb.stylize_batch(prm, cs, gs, lut, frames, frame_seeds=seeds)
+        dct, dco, dlv = sb.stylize_batch(prm, cs, gs, lut, frames)  # default seeds prm.seed + i
+        for i in range(5):
+            p1 = sb.Params(**{**prm.__dict__, "seed": seeds[i]})
+            ct, co, lv = sb.stylize(p1, cs, gs, lut, frames[i])
+            assert torch.equal(ct, bct[i]) and torch.equal(co, bco[i]) and torch.equal(lv, blv[i])
+            p2 = sb.Params(**{**prm.__dict__, "seed": (100 + i) & 0xFFFFFFFF})
+            ct, co, lv = sb.stylize(p2, cs, gs, lut, frames[i])
+            assert torch.equal(ct, dct[i]) and torch.equal(co, dco[i])
+        assert torch.equal(bco[1], bco[2]) or not torch.equal(frames[1], frames[2])
+
+
+def test_oracle_parity_batch_frames():
+    """Per-frame seeds reach the jitter: oracle with the same seed per frame."""
+    cfg = synth.CONFIGS[1]
+    cs, gs = synth.exemplar(cfg)
+    frames = torch.stack([synth.heightfield_normals(64, 64, seed=1, frame=i) for i in range(3)])
+    seeds = [5, 6, 0xDEADBEEF]
+    prm = sb.Params(threshold=cfg["t"], levels=3, blend_radius=0, guide_channels=3, seed=0)
+    gsd = gs.to(DEV)
+    ct, co, lv = sb.stylize_batch(prm, cs.to(DEV), gsd, sb.build_lut(gsd), frames.to(DEV), frame_seeds=seeds)
+    lut = oracle_lut(gs.numpy())
+    for i in range(3):
+        o = oracle.stylize(oracle.Params(t=cfg["t"], L=3, C=3, seed=seeds[i]), cs.numpy(), gs.numpy(), lut,
+                           frames[i].numpy())
+        assert (u32(co[i]) == o[1]).all() and (lv[i].cpu().numpy() == o[2]).all() and (ct[i].cpu().numpy() == o[0]).all()
+
+
+@pytest.mark.parametrize("r", [0, 2])
+def test_strips_equal_whole_frame(r):
+    cfg = synth.CONFIGS[3]
+    cs, gs = [t.to(DEV) for t in synth.exemplar(cfg)]
+    lut = sb.build_lut(gs)
+    gt = synth.heightfield_normals(640, 203, seed=3).to(DEV)
+    prm = sb.Params(threshold=cfg["t"], levels=5, blend_radius=r, guide_channels=3, seed=cfg["seed"])
+    ct, co, lv = sb.stylize(prm, cs, gs, lut, gt)
+    for cuts in ([0, 100, 203], [0, 1, 17, 64, 150, 202, 203], [0, 203]):
+        ct2 = torch.zeros_like(ct)
+        lv2 = torch.zeros_like(lv)
+        co2 = torch.zeros_like(co)
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            p = sb.Params(**{**prm.__dict__, "row_begin": a, "row_end": b})
+            sb.stylize(p, cs, gs, lut, gt, ct=ct2, coords=co2, level=lv2)
+        assert torch.equal(ct, ct2) and torch.equal(lv, lv2) and torch.equal(co, co2)
+
+
+def test_repeatable_and_no_color():
+    cfg = synth.CONFIGS[2]
+    cs, gs = [t.to(DEV) for t in synth.exemplar(cfg)]
+    lut = sb.build_lut(gs)
+    gt = synth.target(2).to(DEV)
+    prm = sb.Params(threshold=cfg["t"], levels=5, blend_radius=2, guide_channels=3, seed=1)
+    a = sb.stylize(prm, cs, gs, lut, gt)
+    b = sb.stylize(prm, cs, gs, lut, gt)
+    assert all(torch.equal(x, y) for x, y in zip(a, b))
+    pn = sb.Params(**{**prm.__dict__, "flags": sb.SB_NO_COLOR})
+    ct, co, lv = sb.stylize(pn, cs, gs, lut, gt)
+    assert ct is None and torch.equal(co, a[1]) and torch.equal(lv, a[2])
+
+
+def test_host_pipeline_equals_device_batch():
+    cfg = synth.CONFIGS[3]
+    cs, gs = [t.to(DEV) for t in synth.exemplar(cfg)]
+    lut = sb.build_lut(gs)
+    frames = torch.stack([synth.heightfield_normals(512, 288, seed=4, frame=i) for i in range(5)])
+    for r in (0, 2):
+        prm = sb.Params(threshold=cfg["t"], levels=5, blend_radius=r, guide_channels=3, seed=9)
+        dct, dco, _ = sb.stylize_batch(prm, cs, gs, lut, frames.to(DEV))
+        gt_h = frames.pin_memory()
+        ct_h = torch.empty_like(gt_h).pin_memory()
+        co_h = torch.empty(5, 288, 512, dtype=torch.int32).pin_memory()
+        sb.stylize_batch_host(prm, cs, gs, lut, gt_h, ct_h, co_h, depth=2)
+        assert torch.equal(ct_h, dct.cpu()) and torch.equal(co_h, dco.cpu())
+
+
+def test_naive_kernel_agrees(tmp_path):
+    """The one-thread-per-pixel kernel (SB_KERNEL=naive) and the tiled kernel agree (run in a
+    subprocess so the environment switch takes effect)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import torch, numpy as np, synth, paper_1807_03249_b200 as sb\n"
+        "cfg=synth.CONFIGS[2]; cs,gs=[t.cuda() for t in synth.exemplar(cfg)]; lut=sb.build_lut(gs)\n"
+        "gt=synth.target(2).cuda()\n"
+        "p=sb.Params(threshold=cfg['t'],levels=5,blend_radius=2,guide_channels=3,seed=4)\n"
+        "ct,co,lv=sb.stylize(p,cs,gs,lut,gt); torch.cuda.synchronize()\n"
+        "np.save(r'%s', np.concatenate([co.cpu().numpy().ravel(), ct.cpu().numpy().view(np.int32).ravel(), lv.cpu().numpy().astype(np.int32).ravel()]))\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for mode in ("tiled", "naive"):
+        f = tmp_path / f"{mode}.npy"
+        env = dict(os.environ, SB_KERNEL=mode, PYTHONPATH=root)
+        subprocess.check_call([sys.executable, "-c", code % f], env=env, cwd=root)
+        outs.append(np.load(f))
+    assert (outs[0] == outs[1]).all()
