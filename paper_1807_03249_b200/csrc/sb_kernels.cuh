@@ -5,6 +5,7 @@
 namespace sb {
 
 constexpr int kSeedsPerLaunch = 512;  // frames per launch (per-frame seeds travel as params)
+#define SB_MAX_LEVELS_DEV 12           // == SB_MAX_LEVELS of include/styleblit.h
 
 struct StylizeArgs {
     const uint8_t* cs;

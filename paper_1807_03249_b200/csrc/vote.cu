@@ -4,114 +4,255 @@
 // target) of C_S[src(q) + (p - q)], skipping positions outside the source; per channel
 // floor((sum + floor(n/2)) / n) (reading R13).  Fallback pixels vote like any other (R14).
 //
-// One CTA = 128 x 16 output pixels; the coordinate field of the tile plus an r-pixel halo is
-// staged in shared memory.  Each pixel first checks whether every window position votes for
-// the same source pixel (the chunk interior, where the paper notes voting equals the blit,
-// PAPER.md:420-421) -- then it is one gather; otherwise it accumulates the (2r+1)^2 gathers
-// with SWAR (two 16-bit lanes per register; (2r+1)^2 * 255 < 2^16 for r <= 7) and divides by
-// n with an exact multiply-high.
+// One CTA = 128 x 16 output pixels, 256 threads; the coordinate field of the tile plus an
+// r-pixel halo is staged in shared memory, the colours are assembled in shared memory and
+// leave in coalesced 16-byte stores.
 //
-// Packed coordinates x | y<<16: for W, H <= 32767 and |d| <= 2r the packed sum
-// src(q) + (p-q) never carries between fields, and any position left of / above the source
-// wraps to a field >= 0xFFF0, which the bounds test rejects.
+// Fast tiles (the common case): every staged position is inside the target and every staged
+// source pixel is at least r from the source border.  Then no window position can be clipped
+// or leave the source, the staged coordinates are converted to linear source indices
+// (y*ws + x), and "q votes for the same source pixel as p" is the linear identity
+// lin(q) - lin(p) = (qx - px) + (qy - py)*ws (exact under the margin).
+//   1. per staged row and 4-pixel group: which of the 4 row segments [x-r, x+r] are one chunk
+//      (a nibble per group, from two 16-byte shared loads);
+//   2. per pixel: the window is one chunk iff its 2r+1 row segments are and the centre column
+//      continues vertically -- then the vote is unanimous and C_T[p] = C_S[src(p)] (the chunk
+//      interior, where voting equals the blit): one gather;
+//   3. the other pixels go to a shared-memory queue, processed densely one pixel per thread:
+//      (2r+1)^2 branch-free gathers summed in SWAR (two 16-bit lanes per register;
+//      (2r+1)^2 * 255 < 2^16 for r <= 7), division by the constant (2r+1)^2.
+// Border tiles: every pixel takes the general per-position path with target clipping and
+// source bounds tests on packed coordinates (x | y<<16; for W, H <= 32767 and |d| <= 2r the
+// packed sum src(q) + (p-q) never carries between fields and any position left of / above
+// the source wraps to a field >= 0xFFF0, which the bounds test rejects).
 #include "sb_kernels.cuh"
 
 namespace sb {
 
 namespace {
 constexpr int TW = 128, TH = 16, NT = 256;
-constexpr uint32_t kOutside = 0xFFFFFFFFu;  // window position outside the target
+constexpr int NG = TW / 4;                   // 4-pixel groups per row
+constexpr uint32_t kOutside = 0xFFFFFFFFu;   // window position outside the target
+
+__device__ __forceinline__ uint32_t finish(uint32_t lo, uint32_t hi, uint32_t n) {
+    if (n <= 1) return (lo & 0x00FF00FFu) | ((hi & 0x00FF00FFu) << 8);
+    const uint32_t half = n >> 1;
+    const uint32_t m = 0xFFFFFFFFu / n + 1u;  // ceil(2^32/n): exact floor for numerators < 2^17
+    const uint32_t c0 = __umulhi((lo & 0xFFFFu) + half, m);
+    const uint32_t c1 = __umulhi((hi & 0xFFFFu) + half, m);
+    const uint32_t c2 = __umulhi((lo >> 16) + half, m);
+    const uint32_t c3 = __umulhi((hi >> 16) + half, m);
+    return c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
+}
+
+template <uint32_t N>
+__device__ __forceinline__ uint32_t finish_const(uint32_t lo, uint32_t hi) {
+    constexpr uint32_t half = N / 2;
+    const uint32_t c0 = ((lo & 0xFFFFu) + half) / N;
+    const uint32_t c1 = ((hi & 0xFFFFu) + half) / N;
+    const uint32_t c2 = ((lo >> 16) + half) / N;
+    const uint32_t c3 = ((hi >> 16) + half) / N;
+    return c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
+}
+
+__device__ __forceinline__ void swar_add(uint32_t c, uint32_t& lo, uint32_t& hi) {
+    lo += c & 0x00FF00FFu;
+    hi += __byte_perm(c, 0u, 0x7371);  // bytes 1 and 3 into 16-bit lanes
+}
 }  // namespace
 
+template <int R>
 __global__ void __launch_bounds__(NT) vote_kernel(const VoteArgs a) {
-    extern __shared__ __align__(16) uint32_t sc[];  // (TH + 2r) x (TW + 2r)
-    const int r = a.r;
-    const int SW = TW + 2 * r;
+    constexpr int SW = TW + 2 * R, SH = TH + 2 * R;
+    constexpr int KR = (R + 3) / 4;           // 16-byte words covering the halo
+    constexpr int OFF = 4 * KR;               // tile column x is stored at sc[.][OFF + x]
+    constexpr int SWP = OFF + TW + OFF;       // 16-byte aligned rows
+    __shared__ __align__(16) uint32_t sc[SH][SWP];
+    __shared__ uint8_t seg[SH][NG];        // nibble: which of the group's 4 row segments are one chunk
+    __shared__ __align__(16) uint32_t outc[TH][TW];
+    __shared__ uint16_t queue[TH * TW];
+    __shared__ int qn;
+
     const int tiles_x = (a.wt + TW - 1) / TW;
     const int x0 = (blockIdx.x % tiles_x) * TW;
     const int y0 = a.row_begin + (blockIdx.x / tiles_x) * TH;
     const int64_t fpx = (int64_t)a.wt * a.ht;
     const uint32_t* __restrict__ cf = a.coords + fpx * blockIdx.y;
     const uint32_t* __restrict__ cs = reinterpret_cast<const uint32_t*>(a.cs);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t ws = (uint32_t)a.ws, hs = (uint32_t)a.hs;
 
-    const int SH = TH + 2 * r;
+    if (threadIdx.x == 0) qn = 0;
+    // ---- stage coords (tile + halo), outside the target -> kOutside; test the fast-tile margin
+    bool fast_mine = true;
     for (int i = threadIdx.x; i < SW * SH; i += NT) {
         const int yy = i / SW, xx = i - yy * SW;
-        const int gx = x0 - r + xx, gy = y0 - r + yy;
+        const int gx = x0 - R + xx, gy = y0 - R + yy;
         uint32_t v = kOutside;
-        if (gx >= 0 && gx < a.wt && gy >= 0 && gy < a.ht) v = __ldg(cf + (int64_t)gy * a.wt + gx);
-        sc[i] = v;
+        if (gx >= 0 && gx < a.wt && gy >= 0 && gy < a.ht) {
+            v = __ldg(cf + (int64_t)gy * a.wt + gx);
+            const uint32_t sx = v & 0xFFFFu, sy = v >> 16;
+            fast_mine &= (sx >= (uint32_t)R) & (sx + (uint32_t)R < ws) & (sy >= (uint32_t)R) & (sy + (uint32_t)R < hs);
+        } else {
+            fast_mine = false;
+        }
+        sc[yy][OFF - R + xx] = v;
+    }
+    const bool fast = __syncthreads_and(fast_mine) != 0;
+
+    const int g = lane;                  // this thread's 4-pixel group column (pixels 4g..4g+3)
+    if (fast) {
+        // ---- packed -> linear source index, in place
+        for (int i = threadIdx.x; i < SW * SH; i += NT) {
+            const int yy = i / SW, xx = i - yy * SW;
+            const uint32_t v = sc[yy][OFF - R + xx];
+            sc[yy][OFF - R + xx] = (v >> 16) * ws + (v & 0xFFFFu);
+        }
+        __syncthreads();
+        if (R > 0) {
+            // ---- 1. row-segment nibbles: tile columns 4g-R .. 4g+3+R of staged row yy
+            for (int e = threadIdx.x; e < SH * NG; e += NT) {
+                const int yy = e / NG, gg = e - yy * NG;
+                uint32_t u[4 * (2 * KR + 1)];  // tile columns 4gg-4KR .. 4gg+3+4KR
+#pragma unroll
+                for (int k = 0; k < 2 * KR + 1; ++k) {
+                    const uint4 t = *reinterpret_cast<const uint4*>(&sc[yy][4 * gg + 4 * k]);
+                    u[4 * k] = t.x; u[4 * k + 1] = t.y; u[4 * k + 2] = t.z; u[4 * k + 3] = t.w;
+                }
+                const uint32_t* v = u + (4 * KR - R);  // v[i] = tile column 4gg - R + i
+                uint32_t link = 0;  // bit i: v[i+1] continues v[i]
+#pragma unroll
+                for (int i = 0; i < 3 + 2 * R; ++i) link |= (uint32_t)(v[i + 1] == v[i] + 1u) << i;
+                constexpr uint32_t win = (1u << (2 * R)) - 1u;
+                uint32_t nib = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) nib |= (uint32_t)(((link >> k) & win) == win) << k;
+                seg[yy][gg] = (uint8_t)nib;
+            }
+            __syncthreads();
+        }
+        // ---- 2. per pixel: unanimous window -> blit, else queue
+        int my_n = 0;
+        uint32_t my_mask = 0;  // bit 4*rr + k: queued
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const int ry = warp + 8 * rr;
+            if (y0 + ry >= a.row_end || x0 + 4 * g >= a.wt) continue;
+            const uint4 c4 = *reinterpret_cast<const uint4*>(&sc[ry + R][OFF + 4 * g]);
+            const uint32_t cp[4] = {c4.x, c4.y, c4.z, c4.w};
+            uint32_t uni = 0xFu;
+#pragma unroll
+            for (int j = -R; j <= R; ++j) {
+                uint32_t m = seg[ry + R + j][g];
+                const uint4 v4 = *reinterpret_cast<const uint4*>(&sc[ry + R + j][OFF + 4 * g]);
+                const uint32_t vv[4] = {v4.x, v4.y, v4.z, v4.w};
+                const uint32_t sh = (uint32_t)j * ws;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) m &= ~((uint32_t)(vv[k] != cp[k] + sh) << k);
+                uni &= (R > 0) ? m : 0xFu;
+            }
+            uint32_t o[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                o[k] = 0;
+                if ((uni >> k) & 1u) o[k] = __ldg(cs + cp[k]);
+                else { my_mask |= 1u << (4 * rr + k); ++my_n; }
+            }
+            *reinterpret_cast<uint4*>(&outc[ry][4 * g]) = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+        int incl = my_n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        int base = 0;
+        if (lane == 31 && total) base = atomicAdd(&qn, total);
+        base = __shfl_sync(0xFFFFFFFFu, base, 31) + incl - my_n;
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+            if (my_mask & (1u << b)) queue[base++] = (uint16_t)((warp + 8 * (b >> 2)) * TW + 4 * g + (b & 3));
+        __syncthreads();
+        // ---- 3. dense per-pixel voting, branch-free
+        const int n = qn;
+        for (int j = threadIdx.x; j < n; j += NT) {
+            const int idx = queue[j];
+            const int ry = idx / TW, x = idx - ry * TW;
+            uint32_t lo = 0, hi = 0;
+#pragma unroll
+            for (int dy = -R; dy <= R; ++dy) {
+                const uint32_t* row = &sc[ry + R + dy][OFF + x];
+                const uint32_t shy = (uint32_t)dy * ws;
+#pragma unroll
+                for (int dx = -R; dx <= R; ++dx) swar_add(__ldg(cs + (row[dx] - shy - (uint32_t)dx)), lo, hi);
+            }
+            outc[ry][x] = finish_const<(2 * R + 1) * (2 * R + 1)>(lo, hi);
+        }
+    } else {
+        // ---- border tile: every pixel takes the general path
+        const int ntile = TH * TW;
+        for (int idx = threadIdx.x; idx < ntile; idx += NT) {
+            const int ry = idx / TW, x = idx - ry * TW;
+            const int gx = x0 + x;
+            if (y0 + ry >= a.row_end || gx >= a.wt) continue;
+            uint32_t lo = 0, hi = 0, cnt = 0;
+#pragma unroll
+            for (int dy = -R; dy <= R; ++dy) {
+                const uint32_t sh = (uint32_t)dy << 16;
+#pragma unroll
+                for (int dx = -R; dx <= R; ++dx) {
+                    const uint32_t w = sc[ry + R + dy][OFF + x + dx];
+                    const uint32_t pos = w - (uint32_t)dx - sh;
+                    const bool in = (w != kOutside) & ((pos & 0xFFFFu) < ws) & ((pos >> 16) < hs);
+                    const uint32_t c = __ldg(cs + (in ? (pos >> 16) * ws + (pos & 0xFFFFu) : 0u));
+                    if (in) { swar_add(c, lo, hi); ++cnt; }
+                }
+            }
+            outc[ry][x] = finish(lo, hi, cnt);  // cnt >= 1: q = p votes for src(p)
+        }
     }
     __syncthreads();
-
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int rx0 = lane * 4;
-    const uint32_t ws = (uint32_t)a.ws, hs = (uint32_t)a.hs;
-#pragma unroll 1
+    // ---- store the tile
+    const bool vec = (a.wt & 3) == 0;
+#pragma unroll
     for (int rr = 0; rr < 2; ++rr) {
         const int ry = warp + 8 * rr;
         const int py = y0 + ry;
-        if (py >= a.row_end || x0 + rx0 >= a.wt) continue;
-        uint32_t outv[4];
+        const int gx0 = x0 + 4 * g;
+        if (py >= a.row_end || gx0 >= a.wt) continue;
+        const int64_t off = fpx * blockIdx.y + (int64_t)py * a.wt + gx0;
+        const uint4 o = *reinterpret_cast<const uint4*>(&outc[ry][4 * g]);
+        if (vec) {
+            st_cs_u4(a.ct + 4 * off, o);
+        } else {
+            const uint32_t ov[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int cx = rx0 + i + r, cy = ry + r;  // p in smem coordinates
-            const uint32_t cp = sc[cy * SW + cx];
-            // pass 1: does every in-target window position vote for src(p)?
-            bool uniform = true;
-            for (int dy = -r; dy <= r; ++dy) {
-                const uint32_t* row = sc + (cy + dy) * SW + cx;
-                const uint32_t sh = (uint32_t)dy << 16;
-                for (int dx = -r; dx <= r; ++dx) {
-                    const uint32_t v = row[dx];
-                    // position voted by q = p + (dx,dy): src(q) - (dx,dy)
-                    uniform &= (v == kOutside) | (v - (uint32_t)dx - sh == cp);
-                }
-            }
-            if (uniform) {
-                outv[i] = __ldg(cs + (cp >> 16) * ws + (cp & 0xFFFFu));
-                continue;
-            }
-            // pass 2: full average
-            uint32_t lo = 0, hi = 0, n = 0;
-            for (int dy = -r; dy <= r; ++dy) {
-                const uint32_t* row = sc + (cy + dy) * SW + cx;
-                const uint32_t sh = (uint32_t)dy << 16;
-                for (int dx = -r; dx <= r; ++dx) {
-                    const uint32_t v = row[dx];
-                    if (v == kOutside) continue;
-                    const uint32_t pos = v - (uint32_t)dx - sh;
-                    const uint32_t sx = pos & 0xFFFFu, sy = pos >> 16;
-                    if (sx >= ws || sy >= hs) continue;
-                    const uint32_t c = __ldg(cs + sy * ws + sx);
-                    lo += c & 0x00FF00FFu;
-                    hi += (c >> 8) & 0x00FF00FFu;
-                    ++n;
-                }
-            }
-            // n >= 1 (q = p votes for src(p), inside the source)
-            const uint32_t half = n >> 1;
-            uint32_t ch[4] = {(lo & 0xFFFFu) + half, (hi & 0xFFFFu) + half, (lo >> 16) + half, (hi >> 16) + half};
-            uint32_t res = 0;
-            if (n == 1) {
-                res = (ch[0] - half) | ((ch[1] - half) << 8) | ((ch[2] - half) << 16) | ((ch[3] - half) << 24);
-            } else {
-                const uint32_t m = 0xFFFFFFFFu / n + 1u;  // ceil(2^32 / n); exact for sums < 2^17
-#pragma unroll
-                for (int c = 0; c < 4; ++c) res |= __umulhi(ch[c], m) << (8 * c);
-            }
-            outv[i] = res;
+            for (int k = 0; k < 4; ++k)
+                if (gx0 + k < a.wt) st_cs_u32(a.ct + 4 * (off + k), ov[k]);
         }
-        const int64_t o = fpx * blockIdx.y + (int64_t)py * a.wt + x0 + rx0;
-        st_cs_u4(a.ct + 4 * o, make_uint4(outv[0], outv[1], outv[2], outv[3]));
     }
+}
+
+template <int R>
+static void launch_r(const VoteArgs& a, dim3 grid, cudaStream_t st) {
+    vote_kernel<R><<<grid, NT, 0, st>>>(a);
 }
 
 cudaError_t launch_vote(const VoteArgs& a, int n_frames, cudaStream_t st, int* launches) {
     const int tiles = ((a.wt + TW - 1) / TW) * ((a.row_end - a.row_begin + TH - 1) / TH);
-    const size_t smem = sizeof(uint32_t) * (TW + 2 * a.r) * (TH + 2 * a.r);
     dim3 grid((unsigned)tiles, (unsigned)n_frames);
-    vote_kernel<<<grid, NT, smem, st>>>(a);
+    switch (a.r) {
+        case 0: launch_r<0>(a, grid, st); break;
+        case 1: launch_r<1>(a, grid, st); break;
+        case 2: launch_r<2>(a, grid, st); break;
+        case 3: launch_r<3>(a, grid, st); break;
+        case 4: launch_r<4>(a, grid, st); break;
+        case 5: launch_r<5>(a, grid, st); break;
+        case 6: launch_r<6>(a, grid, st); break;
+        case 7: launch_r<7>(a, grid, st); break;
+        default: return cudaErrorInvalidValue;
+    }
     *launches += 1;
     return cudaPeekAtLastError();
 }
