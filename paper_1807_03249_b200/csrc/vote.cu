@@ -14,7 +14,7 @@
 // (y*ws + x), and "q votes for the same source pixel as p" is the linear identity
 // lin(q) - lin(p) = (qx - px) + (qy - py)*ws (exact under the margin).
 //   1. per staged row and 4-pixel group: which of the 4 row segments [x-r, x+r] are one chunk
-//      (a nibble per group, from two 16-byte shared loads);
+//      (a nibble per group, from 16-byte shared loads);
 //   2. per pixel: the window is one chunk iff its 2r+1 row segments are and the centre column
 //      continues vertically -- then the vote is unanimous and C_T[p] = C_S[src(p)] (the chunk
 //      interior, where voting equals the blit): one gather;
@@ -62,7 +62,7 @@ __device__ __forceinline__ void swar_add(uint32_t c, uint32_t& lo, uint32_t& hi)
 }  // namespace
 
 template <int R>
-__global__ void __launch_bounds__(NT) vote_kernel(const VoteArgs a) {
+__global__ void __launch_bounds__(NT, (R <= 3 ? 8 : 2)) vote_kernel(const VoteArgs a) {
     constexpr int SW = TW + 2 * R, SH = TH + 2 * R;
     constexpr int KR = (R + 3) / 4;           // 16-byte words covering the halo
     constexpr int OFF = 4 * KR;               // tile column x is stored at sc[.][OFF + x]
@@ -85,28 +85,72 @@ __global__ void __launch_bounds__(NT) vote_kernel(const VoteArgs a) {
     if (threadIdx.x == 0) qn = 0;
     // ---- stage coords (tile + halo), outside the target -> kOutside; test the fast-tile margin
     bool fast_mine = true;
-    for (int i = threadIdx.x; i < SW * SH; i += NT) {
-        const int yy = i / SW, xx = i - yy * SW;
-        const int gx = x0 - R + xx, gy = y0 - R + yy;
-        uint32_t v = kOutside;
-        if (gx >= 0 && gx < a.wt && gy >= 0 && gy < a.ht) {
-            v = __ldg(cf + (int64_t)gy * a.wt + gx);
+    auto stage = [&](int yy, int x, uint32_t v, bool in) {  // x: tile column (-R .. TW-1+R)
+        if (in) {
             const uint32_t sx = v & 0xFFFFu, sy = v >> 16;
             fast_mine &= (sx >= (uint32_t)R) & (sx + (uint32_t)R < ws) & (sy >= (uint32_t)R) & (sy + (uint32_t)R < hs);
         } else {
+            v = kOutside;
             fast_mine = false;
         }
-        sc[yy][OFF - R + xx] = v;
+        sc[yy][OFF + x] = v;
+    };
+    if ((a.wt & 3) == 0) {
+        // centre columns: one 16-byte load per 4 pixels
+        for (int i = threadIdx.x; i < SH * NG; i += NT) {
+            const int yy = i / NG, gg = i - yy * NG;
+            const int gx = x0 + 4 * gg, gy = y0 - R + yy;
+            const bool rowin = gy >= 0 && gy < a.ht;
+            if (rowin && gx + 3 < a.wt) {
+                const uint4 v = *reinterpret_cast<const uint4*>(cf + (int64_t)gy * a.wt + gx);
+                uint32_t m = 0;
+                const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t sx = vv[k] & 0xFFFFu, sy = vv[k] >> 16;
+                    m |= (uint32_t)((sx < (uint32_t)R) | (sx + (uint32_t)R >= ws) | (sy < (uint32_t)R) |
+                                    (sy + (uint32_t)R >= hs));
+                }
+                fast_mine &= (m == 0);
+                *reinterpret_cast<uint4*>(&sc[yy][OFF + 4 * gg]) = v;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const bool in = rowin && gx + k < a.wt;
+                    stage(yy, 4 * gg + k, in ? __ldg(cf + (int64_t)gy * a.wt + gx + k) : 0u, in);
+                }
+            }
+        }
+        // halo columns
+        for (int i = threadIdx.x; i < SH * 2 * R; i += NT) {
+            const int yy = i / (2 * R), k = i - yy * (2 * R);
+            const int x = k < R ? k - R : TW + (k - R);
+            const int gx = x0 + x, gy = y0 - R + yy;
+            const bool in = gx >= 0 && gx < a.wt && gy >= 0 && gy < a.ht;
+            stage(yy, x, in ? __ldg(cf + (int64_t)gy * a.wt + gx) : 0u, in);
+        }
+    } else {
+        for (int i = threadIdx.x; i < SW * SH; i += NT) {
+            const int yy = i / SW, xx = i - yy * SW;
+            const int gx = x0 - R + xx, gy = y0 - R + yy;
+            const bool in = gx >= 0 && gx < a.wt && gy >= 0 && gy < a.ht;
+            stage(yy, xx - R, in ? __ldg(cf + (int64_t)gy * a.wt + gx) : 0u, in);
+        }
     }
     const bool fast = __syncthreads_and(fast_mine) != 0;
 
     const int g = lane;                  // this thread's 4-pixel group column (pixels 4g..4g+3)
     if (fast) {
-        // ---- packed -> linear source index, in place
-        for (int i = threadIdx.x; i < SW * SH; i += NT) {
-            const int yy = i / SW, xx = i - yy * SW;
-            const uint32_t v = sc[yy][OFF - R + xx];
-            sc[yy][OFF - R + xx] = (v >> 16) * ws + (v & 0xFFFFu);
+        // ---- packed -> linear source index, in place (16 bytes at a time; the unused
+        //      padding words are converted too, harmlessly)
+        for (int i = threadIdx.x; i < SH * (SWP / 4); i += NT) {
+            const int yy = i / (SWP / 4), c4 = i - yy * (SWP / 4);
+            uint4 v = *reinterpret_cast<const uint4*>(&sc[yy][4 * c4]);
+            v.x = (v.x >> 16) * ws + (v.x & 0xFFFFu);
+            v.y = (v.y >> 16) * ws + (v.y & 0xFFFFu);
+            v.z = (v.z >> 16) * ws + (v.z & 0xFFFFu);
+            v.w = (v.w >> 16) * ws + (v.w & 0xFFFFu);
+            *reinterpret_cast<uint4*>(&sc[yy][4 * c4]) = v;
         }
         __syncthreads();
         if (R > 0) {

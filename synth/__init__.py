@@ -6,9 +6,12 @@ CPU oracle (tests) are fed the same bytes produced here.
 
 Fields are evaluated with torch so large batches (4K frames) can be generated on the
 GPU outside any timed region; random parameters come from numpy's seeded RNG, so the
-parameters are identical on every device (the bytes may differ by float rounding
-between CPU and GPU, which never matters: parity always feeds one set of bytes to both
-sides).
+parameters are identical on every device.  Everything is computed in float64: torch's
+float32 transcendental kernels round differently in vectorised and scalar tail paths
+(which depend on memory alignment), which made a few bytes differ between processes; in
+float64 a value would have to land within ~1e-16 of a rounding boundary to flip.  (The
+bytes may still differ between CPU and GPU, which never matters: parity always feeds one
+set of bytes to both sides.)
 
 Generators:
   G1 sphere_normal       -- the "lit sphere" exemplar guide
@@ -37,8 +40,8 @@ def _enc(n: torch.Tensor) -> torch.Tensor:
 
 
 def _grid(W: int, H: int, device) -> tuple[torch.Tensor, torch.Tensor]:
-    y = torch.arange(H, device=device, dtype=torch.float32).view(H, 1).expand(H, W)
-    x = torch.arange(W, device=device, dtype=torch.float32).view(1, W).expand(H, W)
+    y = torch.arange(H, device=device, dtype=torch.float64).view(H, 1).expand(H, W)
+    x = torch.arange(W, device=device, dtype=torch.float64).view(1, W).expand(H, W)
     return x, y
 
 
@@ -59,7 +62,7 @@ def sphere_normal(W: int, H: int, device="cpu") -> torch.Tensor:
 
 
 def _value_noise(W: int, H: int, rng: np.random.RandomState, cells: int, device) -> torch.Tensor:
-    g = torch.from_numpy(rng.rand(cells + 1, cells + 1).astype(np.float32)).to(device)
+    g = torch.from_numpy(rng.rand(cells + 1, cells + 1)).to(device)
     x, y = _grid(W, H, device)
     fx, fy = x / max(W - 1, 1) * cells, y / max(H - 1, 1) * cells
     ix, iy = torch.clamp(fx.floor().long(), 0, cells - 1), torch.clamp(fy.floor().long(), 0, cells - 1)
@@ -76,7 +79,7 @@ def painted_style(W: int, H: int, seed: int = 11, device="cpu") -> torch.Tensor:
     rng = np.random.RandomState(seed)
     x, y = _grid(W, H, device)
     noise = sum(_value_noise(W, H, rng, c, device) * w for c, w in ((4, 0.5), (16, 0.3), (64, 0.2)))
-    strokes = torch.zeros(H, W, device=device)
+    strokes = torch.zeros(H, W, device=device, dtype=torch.float64)
     for _ in range(24):
         ang = rng.uniform(0, math.pi)
         freq = rng.uniform(0.05, 0.25)
@@ -86,8 +89,8 @@ def painted_style(W: int, H: int, seed: int = 11, device="cpu") -> torch.Tensor:
     cx, cy, R = (W - 1) / 2.0, (H - 1) / 2.0, 0.48 * min(W, H)
     r2 = ((x - cx) / R) ** 2 + ((y - cy) / R) ** 2
     nz = torch.sqrt(torch.clamp(1.0 - r2, min=0.0))
-    base = np.array([rng.uniform(0.1, 0.3), rng.uniform(0.2, 0.4), rng.uniform(0.5, 0.8)], np.float32)
-    hi = np.array([rng.uniform(0.8, 1.0), rng.uniform(0.7, 0.9), rng.uniform(0.3, 0.6)], np.float32)
+    base = np.array([rng.uniform(0.1, 0.3), rng.uniform(0.2, 0.4), rng.uniform(0.5, 0.8)], np.float64)
+    hi = np.array([rng.uniform(0.8, 1.0), rng.uniform(0.7, 0.9), rng.uniform(0.3, 0.6)], np.float64)
     shade = torch.clamp(0.15 + 0.85 * nz + 0.35 * (noise - 0.5) + strokes, 0, 1)
     out = torch.empty(H, W, 4, dtype=torch.uint8, device=device)
     for c in range(3):
@@ -115,8 +118,8 @@ def heightfield_normals(W: int, H: int, seed: int = 3, frame: int = 0, device="c
     rng = np.random.RandomState(seed)
     x, y = _grid(W, H, device)
     S = float(min(W, H))
-    zx = torch.zeros(H, W, device=device)
-    zy = torch.zeros(H, W, device=device)
+    zx = torch.zeros(H, W, device=device, dtype=torch.float64)
+    zy = torch.zeros(H, W, device=device, dtype=torch.float64)
     for _ in range(12):
         cx, cy = rng.uniform(0, W), rng.uniform(0, H)
         s = rng.uniform(0.05, 0.2) * S
@@ -151,10 +154,10 @@ def render_objects(W: int, H: int, seed: int = 2, device="cpu") -> torch.Tensor:
     rng = np.random.RandomState(seed)
     x, y = _grid(W, H, device)
     S = float(min(W, H))
-    depth = torch.full((H, W), -1e9, device=device)
-    nx = torch.zeros(H, W, device=device)
-    ny = torch.zeros(H, W, device=device)
-    nz = torch.ones(H, W, device=device)
+    depth = torch.full((H, W), -1e9, device=device, dtype=torch.float64)
+    nx = torch.zeros(H, W, device=device, dtype=torch.float64)
+    ny = torch.zeros(H, W, device=device, dtype=torch.float64)
+    nz = torch.ones(H, W, device=device, dtype=torch.float64)
     for _ in range(5):  # spheres
         cx, cy, R, cz = rng.uniform(0.15, 0.85) * W, rng.uniform(0.15, 0.85) * H, rng.uniform(0.08, 0.25) * S, rng.uniform(0, 1)
         dx, dy = (x - cx) / R, (cy - y) / R
@@ -202,8 +205,8 @@ def warp_uv(W: int, H: int, seed: int = 4, n_rbf: int = 8, amp: float = 40.0,
     rng = np.random.RandomState(seed)
     x, y = _grid(W, H, device)
     scale = min(W, H) / 1024.0
-    dx = torch.zeros(H, W, device=device)
-    dy = torch.zeros(H, W, device=device)
+    dx = torch.zeros(H, W, device=device, dtype=torch.float64)
+    dy = torch.zeros(H, W, device=device, dtype=torch.float64)
     s = sigma * scale
     for _ in range(n_rbf):
         cx, cy = rng.uniform(0, W), rng.uniform(0, H)

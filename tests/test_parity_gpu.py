@@ -280,4 +280,32 @@ def test_naive_kernel_agrees(tmp_path):
         env = dict(os.environ, SB_KERNEL=mode, PYTHONPATH=root)
         subprocess.check_call([sys.executable, "-c", code % f], env=env, cwd=root)
         outs.append(np.load(f))
-    assert (outs[0] == outs[1]).all()
+    if not (outs[0] == outs[1]).all():
+        n = outs[0].size // 3  # coords, ct, level: n each
+        names = ["coords", "ct", "level"]
+        bad = np.nonzero(outs[0] != outs[1])[0]
+        where = [names[min(i // n, 2)] for i in bad[:10]]
+        raise AssertionError(f"{bad.size} mismatches; first {bad[:10].tolist()} in {where}: "
+                             f"tiled {outs[0][bad[:10]].tolist()} naive {outs[1][bad[:10]].tolist()}")
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3])
+@pytest.mark.parametrize("r", [0, 2])
+def test_outputs_fully_written(cid, r):
+    """Every output element is written: two runs into buffers pre-filled with different bytes
+    give identical results (catches unwritten pixels and reads of uninitialised memory)."""
+    cfg = synth.CONFIGS[cid]
+    cs, gs = [t.to(DEV) for t in synth.exemplar(cfg)]
+    lut = sb.build_lut(gs)
+    gt = synth.target(cid).to(DEV)
+    H, W = gt.shape[:2]
+    prm = sb.Params(threshold=cfg["t"], levels=cfg["L"], blend_radius=r, guide_channels=cfg["C"], seed=cfg["seed"])
+    res = []
+    for fill in (0x00, 0xA5):
+        ct = torch.full((H, W, 4), fill, dtype=torch.uint8, device=DEV)
+        co = torch.full((H, W), -1 if fill else 0, dtype=torch.int32, device=DEV)
+        lv = torch.full((H, W), fill, dtype=torch.uint8, device=DEV)
+        sb.stylize(prm, cs, gs, lut, gt, ct=ct, coords=co, level=lv)
+        res.append((ct, co, lv))
+    for a_, b_ in zip(*res):
+        assert torch.equal(a_, b_)
