@@ -43,6 +43,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--frames", type=int, default=64, help="4K frames per GPU per step")
     ap.add_argument("--blend-radius", type=int, default=2)
+    ap.add_argument("--mode", default="frame", choices=["frame", "strip"],
+                    help="frame: each GPU stylizes its own frames (weak scaling, no collective); "
+                         "strip: every frame is split into row strips across GPUs and the C_T strips "
+                         "are gathered to rank 0 with NCCL each step")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -132,6 +136,7 @@ def run_ours(args):
 
     import paper_1807_03249_b200 as sb
     import synth
+    from paper_1807_03249_b200 import sharding
 
     rank, world, local = dist_env()
     if world > 1:
@@ -151,20 +156,30 @@ def run_ours(args):
     for i in range(n_distinct, B):
         gt[i] = gt[i % n_distinct]
     del base
-    seeds = [(cfg["seed"] + rank * B + i) & 0xFFFFFFFF for i in range(B)]
+    strip = args.mode == "strip"
+    if strip:  # all ranks work on the same frames, each on its own row strip
+        for i in range(n_distinct):
+            gt[i] = synth.heightfield_normals(WT, HT, seed=5, frame=i, device=dev)
+        for i in range(n_distinct, B):
+            gt[i] = gt[i % n_distinct]
+    rb, re_ = sharding.strip_rows(HT, world, rank) if strip else (0, HT)
+    frame0 = 0 if strip else rank * B
+    seeds = [(cfg["seed"] + frame0 + i) & 0xFFFFFFFF for i in range(B)]
     coords = torch.empty(B, HT, WT, dtype=torch.int32, device=dev)
     ct = torch.empty(B, HT, WT, 4, dtype=torch.uint8, device=dev)
     lut = torch.empty(65536, dtype=torch.int32, device=dev)
     lut_ws = torch.empty(65536 * 4, dtype=torch.uint8, device=dev)
+    r_halo = r if strip else 0
     prm = sb.Params(threshold=cfg["t"], levels=cfg["L"], blend_radius=0, guide_channels=cfg["C"],
-                    seed=cfg["seed"], flags=sb.SB_NO_COLOR)
+                    seed=cfg["seed"], flags=sb.SB_NO_COLOR, row_begin=max(0, rb - r_halo),
+                    row_end=min(HT, re_ + r_halo))
     stream = torch.cuda.current_stream(dev)
 
-    ev = {k: [] for k in ("lut", "stylize", "vote")}
+    ev = {k: [] for k in ("lut", "stylize", "vote", "gather")}
     launches = [0]
 
     def step(record: bool):
-        es = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if record else None
+        es = [torch.cuda.Event(enable_timing=True) for _ in range(5)] if record else None
         if record:
             es[0].record(stream)
         sb.build_lut(gs, lut, lut_ws)
@@ -175,13 +190,18 @@ def run_ours(args):
         n_s = sb.launch_count()
         if record:
             es[2].record(stream)
-        sb.vote(coords, cs, r, ct=ct)
+        sb.vote(coords, cs, r, ct=ct, row_begin=rb, row_end=re_)
         n_v = sb.launch_count()
         if record:
             es[3].record(stream)
+        if strip and world > 1:  # the one exchange step: C_T strips -> rank 0 over NCCL
+            sharding.gather_strips(ct[:, rb:re_], HT, world, rank, dst=0, row_axis=1)
+        if record:
+            es[4].record(stream)
             ev["lut"].append((es[0], es[1]))
             ev["stylize"].append((es[1], es[2]))
             ev["vote"].append((es[2], es[3]))
+            ev["gather"].append((es[3], es[4]))
             launches[0] += n_l + n_s + n_v
 
     for _ in range(args.warmup):
@@ -207,8 +227,9 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     ms_step = ms / args.steps
-    px_step = B * WT * HT
-    value = world * px_step / (ms_step * 1e-3) / 1e6  # MP/s, whole job
+    px_step = B * WT * HT if not strip else B * WT * (re_ - rb)  # pixels this rank outputs
+    px_job = world * B * WT * HT if not strip else B * WT * HT
+    value = px_job / (ms_step * 1e-3) / 1e6  # MP/s, whole job
 
     kt = {k: statistics.mean(a.elapsed_time(b) for a, b in v) for k, v in ev.items()}
     hbm, hbm_src = peaks()
@@ -217,12 +238,24 @@ def run_ours(args):
     alg = {"stylize": 8 * px_step, "vote": 8 * px_step, "lut": gs.numel() + 65536 * 4}
     dom = max(("stylize", "vote"), key=lambda k: kt[k])
     ach = alg[dom] / (kt[dom] * 1e-3) / 1e9
+    # measured DRAM traffic of the same kernel: one `ncu --set full` capture (profiles/traffic.json,
+    # written by tools/ncu_traffic.py), per pixel, scaled to this launch
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = round(json.load(f)[dom]["bytes_per_px"] * px_step)
+    except Exception:
+        pass
     kernels = {k: {"ms_per_launch": round(kt[k], 4), "share": round(kt[k] / ms_step, 4),
-                   "GBps_alg": round(alg[k] / (kt[k] * 1e-3) / 1e9, 1)} for k in kt}
+                   "GBps_alg": round(alg[k] / (kt[k] * 1e-3) / 1e9, 1)} for k in kt if k in alg}
+    if strip and world > 1:
+        gbytes = (world - 1) * B * WT * (HT // world) * 4  # strips arriving at rank 0
+        kernels["gather"] = {"ms_per_step": round(kt["gather"], 4), "share": round(kt["gather"] / ms_step, 4),
+                             "GBps_into_rank0": round(gbytes / (kt["gather"] * 1e-3) / 1e9, 1)}
 
     # ---- e2e through the host-buffer ABI call (pinned host memory, copies inside timing)
     e2e = None
-    if not args.no_e2e and args.e2e_steps > 0:
+    if not args.no_e2e and args.e2e_steps > 0 and not strip:
         Be = min(B, 16)
         gt_h = gt[:Be].cpu().pin_memory()
         ct_h = torch.empty_like(gt_h).pin_memory()
@@ -264,19 +297,21 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": round(ms_step, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "weak" if not strip else "strong",
         "vs_baseline": None,
         "dtype": "u8",
         "data": "synthetic (seeded heightfield-normal 4K frames, sphere-normal exemplar, painted style)",
         "config": {"workload": f"cfg5: {B} x 4K UHD (3840x2160) frames per GPU, 512x512 exemplar, L={cfg['L']}, "
                                f"t={cfg['t']}, C={cfg['C']}, blend r={r}; step = LUT build + stylize + vote",
                    "frames_per_gpu": B, "global_frames": B * world, "levels": cfg["L"], "threshold": cfg["t"],
-                   "blend_radius": r, "parallelism": f"frame-sharded x{world} (no data-path collective)",
+                   "blend_radius": r,
+                   "parallelism": (f"frame-sharded x{world} (no data-path collective)" if not strip else
+                                   f"row-strip-sharded x{world}, C_T strips gathered to rank 0 (NCCL gather)"),
                    "l2": "inputs larger than L2 (G_T %.2f GB per GPU per step); no flush" % (4 * px_step / 1e9)},
         "fps_4k": round(value * 1e6 / (WT * HT), 1),
         "kernels": kernels,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                     "frac": round(ach / hbm, 4), "traffic": None, "peak_source": hbm_src,
+                     "frac": round(ach / hbm, 4), "traffic": traffic, "peak_source": hbm_src,
                      "alg_bytes_per_launch": alg[dom], "alg_bytes_per_px": 8},
         "gpu_launches": launches[0],
         "clocks": clk.summary(),

@@ -18,9 +18,11 @@
 //   2. per pixel: the window is one chunk iff its 2r+1 row segments are and the centre column
 //      continues vertically -- then the vote is unanimous and C_T[p] = C_S[src(p)] (the chunk
 //      interior, where voting equals the blit): one gather;
-//   3. the other pixels go to a shared-memory queue, processed densely one pixel per thread:
-//      (2r+1)^2 branch-free gathers summed in SWAR (two 16-bit lanes per register;
-//      (2r+1)^2 * 255 < 2^16 for r <= 7), division by the constant (2r+1)^2.
+//   3. the other pixels go to a shared-memory queue, processed densely one pixel per thread,
+//      window row by window row: the row-link bits split a row into runs of positions that
+//      vote for the same source pixel, and each run costs one gather weighted by its length
+//      (typically 1-2 runs per row instead of 2r+1 gathers).  Sums are SWAR (two 16-bit
+//      lanes per register; (2r+1)^2 * 255 < 2^16 for r <= 7); division by (2r+1)^2.
 // Border tiles: every pixel takes the general per-position path with target clipping and
 // source bounds tests on packed coordinates (x | y<<16; for W, H <= 32767 and |d| <= 2r the
 // packed sum src(q) + (p-q) never carries between fields and any position left of / above
@@ -69,6 +71,7 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 8 : 2)) vote_kernel(const VoteAr
     constexpr int SWP = OFF + TW + OFF;       // 16-byte aligned rows
     __shared__ __align__(16) uint32_t sc[SH][SWP];
     __shared__ uint8_t seg[SH][NG];        // nibble: which of the group's 4 row segments are one chunk
+    __shared__ uint32_t hl[SH][6];         // row link bits: bit x+32 <=> position x+1 continues x
     __shared__ __align__(16) uint32_t outc[TH][TW];
     __shared__ uint16_t queue[TH * TW];
     __shared__ int qn;
@@ -172,6 +175,14 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 8 : 2)) vote_kernel(const VoteAr
 #pragma unroll
                 for (int k = 0; k < 4; ++k) nib |= (uint32_t)(((link >> k) & win) == win) << k;
                 seg[yy][gg] = (uint8_t)nib;
+                // assemble the row's link words (a warp holds one staged row: lane == group)
+                uint32_t wv = ((link >> R) & 0xFu) << (4 * (gg & 7));
+                wv |= __shfl_xor_sync(0xFFFFFFFFu, wv, 1);
+                wv |= __shfl_xor_sync(0xFFFFFFFFu, wv, 2);
+                wv |= __shfl_xor_sync(0xFFFFFFFFu, wv, 4);
+                if ((gg & 7) == 0) hl[yy][1 + (gg >> 3)] = wv;
+                if (gg == 0) hl[yy][0] = (link & ((1u << R) - 1u)) << (32 - R);
+                if (gg == NG - 1) hl[yy][5] = (link >> (R + 4)) & ((1u << (R - 1)) - 1u);
             }
             __syncthreads();
         }
@@ -218,20 +229,41 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 8 : 2)) vote_kernel(const VoteAr
         for (int b = 0; b < 8; ++b)
             if (my_mask & (1u << b)) queue[base++] = (uint16_t)((warp + 8 * (b >> 2)) * TW + 4 * g + (b & 3));
         __syncthreads();
-        // ---- 3. dense per-pixel voting, branch-free
+        // ---- 3. dense per-pixel voting by runs: within a window row, consecutive positions
+        //      whose offsets agree (the row-link bits) vote for the same source pixel, so each
+        //      run costs one gather weighted by its length.
         const int n = qn;
         for (int j = threadIdx.x; j < n; j += NT) {
             const int idx = queue[j];
             const int ry = idx / TW, x = idx - ry * TW;
             uint32_t lo = 0, hi = 0;
+            constexpr uint32_t W = 2 * R + 1;
 #pragma unroll
             for (int dy = -R; dy <= R; ++dy) {
-                const uint32_t* row = &sc[ry + R + dy][OFF + x];
+                const int yy = ry + R + dy;
+                const uint32_t b = (uint32_t)(x - R + 32);
+                const uint32_t bits = __funnelshift_r(hl[yy][b >> 5], hl[yy][(b >> 5) + 1], b & 31u);
+                uint32_t m = ~bits & ((1u << (2 * R)) - 1u);  // bit i: a run ends at window position i
+                const uint32_t* row = &sc[yy][OFF + x - R];
                 const uint32_t shy = (uint32_t)dy * ws;
-#pragma unroll
-                for (int dx = -R; dx <= R; ++dx) swar_add(__ldg(cs + (row[dx] - shy - (uint32_t)dx)), lo, hi);
+                uint32_t start = 0;
+                uint32_t pos = row[0] - shy + (uint32_t)R;
+                while (m) {
+                    const uint32_t k = __ffs(m) - 1;
+                    const uint32_t c = __ldg(cs + pos);
+                    const uint32_t len = k + 1 - start;
+                    lo += (c & 0x00FF00FFu) * len;
+                    hi += __byte_perm(c, 0u, 0x7371) * len;
+                    start = k + 1;
+                    m &= m - 1;
+                    pos = row[start] - shy - (start - (uint32_t)R);
+                }
+                const uint32_t c = __ldg(cs + pos);
+                const uint32_t len = W - start;
+                lo += (c & 0x00FF00FFu) * len;
+                hi += __byte_perm(c, 0u, 0x7371) * len;
             }
-            outc[ry][x] = finish_const<(2 * R + 1) * (2 * R + 1)>(lo, hi);
+            outc[ry][x] = finish_const<W * W>(lo, hi);
         }
     } else {
         // ---- border tile: every pixel takes the general path
