@@ -1,8 +1,9 @@
 // stylize.cu -- tiled Alg. 2 "ParallelStyleBlit" for sm_100a.
 //
-// One CTA = one 128 x 16 pixel tile of one frame (256 threads, 4 consecutive pixels x 2 rows
-// per thread, uint4 I/O).  Per tile and level l the seed cells that any tile pixel can reach
-// (its 3x3 neighbourhood) are materialised in shared memory:
+// One CTA = one 128 x 32 pixel tile of one frame (grid = tiles_x x tiles_y x frames), 256
+// threads; warp w owns tile rows w, w+8, w+16, w+24 and a thread owns 4 consecutive pixels of
+// each (uint4 I/O).  Per tile and level l the seed cells that any tile pixel can reach (its
+// 3x3 neighbourhood) are materialised in shared memory:
 //     cell = (4*(s.x - x0), 4*(s.y - y0), delta),  delta = u* - q packed as dy*65536 + dx,
 // where s is the jittered seed (SeedPoint, lines 354-358), q = clamp(s) (reading R8) and
 // u* = LUT[G_T[q]] (line 383).  A pixel's candidate is then s = p + delta of its nearest seed
@@ -12,12 +13,13 @@
 // Levels run coarse to fine with compaction:
 //   level L    every 4-pixel group (the pixels of a 4-aligned group share their cell for
 //              h >= 4, so the 9 seed loads and the dy terms are shared by 4 pixels);
-//   level L-1  only the groups with a rejected pixel, densely from a group queue, same
-//              shared-cell evaluation;
-//   below      the remaining pixels from a pixel queue, one per thread; the table of a level
-//              is built only when enough pixels reach it (n*5 >= cells), otherwise its few
-//              pixels evaluate their 9 seeds straight from the hash.
-// Tables of levels L, L-1 (and L-2 when h >= 4 there) are built together up front.  Pixels
+//   level L-1  only the groups with a rejected pixel, densely from a warp-local group list,
+//              same shared-cell evaluation;
+//   below      the remaining pixels from a warp-local pixel queue, one per lane.
+// The tables of the levels L, L-1, L-2 that have h >= 4 are built together up front, behind
+// the kernel's only CTA barrier; afterwards each warp works on its own rows with warp-local
+// lists (ballot/scan compaction, __syncwarp only), so warps never wait for each other.  Levels
+// without a table (h = 2, or below L-2) evaluate their 9 seeds straight from the hash.  Pixels
 // left after level 1 take the level-0 look-up (reading R12).
 //
 // NearestSeed ties: key = 16*d + i, i = 3*(x+1) + (y+1) in Alg. 2's loop order (x outer, y
@@ -29,24 +31,24 @@ namespace sb {
 
 namespace {
 constexpr int TW = 128;           // tile width  (pixels)
-constexpr int TH = 16;            // tile height (pixels)
+constexpr int TH = 32;            // tile height (pixels)
 constexpr int NT = 256;           // threads per CTA
 constexpr int TP = TW * TH;       // pixels per tile
 constexpr int NG = TW / 4;        // 4-pixel groups per row
-// cells of levels 1 and 2 together bound every table set the kernel keeps at once
-constexpr int CELLS1 = (TW / 2 + 3) * (TH / 2 + 3);
-constexpr int CELLS2 = (TW / 4 + 3) * (TH / 4 + 3);
-constexpr int MAXCELLS = CELLS1 + CELLS2;
+constexpr int NW = NT / 32;       // warps per CTA
+constexpr int RPW = TH / NW;      // rows per warp (w, w + 8, ...)
+constexpr int WPX = TP / NW;      // pixels per warp
+// tables kept at once: levels {L, L-1, L-2} with h >= 4, i.e. at most levels 4, 3, 2
+constexpr int cells_of(int h) { return (TW / h + 3) * (TH / h + 3); }
+constexpr int MAXCELLS = cells_of(4) + cells_of(8) + cells_of(16);
 
 struct Smem {
-    uint32_t gt[TP];          // G_T tile
-    uint32_t coord[TP];       // result coords
-    uint8_t lvl[TP];          // result levels
-    uint16_t q[2][TP];        // pixel queues (tile-local index y*TW + x); q[0] doubles as group queue
-    uint8_t gmask[TH * NG];   // per group: pixels still rejected after level L
-    int4 cell[MAXCELLS];      // seed/offset tables, row-major per level (ci*ncy + cj)
-    int offtab[4][16];        // winner offsets per table slot (L, L-1, L-2, finer)
-    int qn[SB_MAX_LEVELS_DEV + 2];  // appended entries per level
+    uint32_t coord[TP];           // result coords
+    uint8_t lvl[TP];              // result levels
+    uint16_t wq[NW][WPX];         // per-warp pixel queue (compacted in place)
+    uint16_t glist[NW][RPW * NG]; // per-warp list of groups with a rejected pixel
+    int4 cell[MAXCELLS];          // seed/offset tables, row-major per level (ci*ncy + cj)
+    int offtab[3][16];            // winner offsets per table slot (L, L-1, L-2)
 };
 
 struct CellGrid {
@@ -85,19 +87,17 @@ __device__ __forceinline__ void write_offtab(int* tab, int ncy) {
 
 __device__ __forceinline__ uint32_t min3u(uint32_t a, uint32_t b, uint32_t c) { return min(min(a, b), c); }
 
-// Warp-aggregated reservation of n_mine slots of counter *cnt; returns this lane's first slot.
-__device__ __forceinline__ int warp_reserve(int* cnt, int n_mine) {
+// Exclusive warp prefix sum of v; *total receives the warp-wide sum.
+__device__ __forceinline__ int warp_excl_scan(int v, int* total) {
     const int lane = threadIdx.x & 31;
-    int incl = n_mine;
+    int incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= o) incl += v;
+        const int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += t;
     }
-    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-    int base = 0;
-    if (lane == 31 && total) base = atomicAdd(cnt, total);
-    return __shfl_sync(0xFFFFFFFFu, base, 31) + incl - n_mine;
+    *total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    return incl - v;
 }
 
 // Candidate test of Alg. 2 lines 384-385 on the packed candidate c = s.x | s.y<<16:
@@ -148,271 +148,247 @@ __device__ __forceinline__ uint32_t group_eval(const Smem& sm, const StylizeArgs
     return acc;
 }
 
+// Alg. 2 at level l for one pixel from the level's shared-memory table.
+__device__ __forceinline__ uint32_t table_candidate(const Smem& sm, const CellGrid& g, const int* offtab, int l,
+                                                    int x0, int y0, int rx, int ry) {
+    const int px = x0 + rx, py = y0 + ry;
+    const int base = g.off + ((px >> l) - g.cx0) * g.ncy + ((py >> l) - g.cy0);
+    const int R4x = 4 * rx, R4y = 4 * ry;
+    uint32_t kk[3];
+#pragma unroll
+    for (int x = -1; x <= 1; ++x) {
+        uint32_t kx[3];
+#pragma unroll
+        for (int y = -1; y <= 1; ++y) {
+            const int2 s = *reinterpret_cast<const int2*>(&sm.cell[base + x * g.ncy + y]);
+            const int dx4 = s.x - R4x, dy4 = s.y - R4y;
+            kx[y + 1] = (uint32_t)(dx4 * dx4) + (uint32_t)(dy4 * dy4) + (uint32_t)(3 * (x + 1) + (y + 1));
+        }
+        kk[x + 1] = min3u(kx[0], kx[1], kx[2]);
+    }
+    const uint32_t key = min3u(kk[0], kk[1], kk[2]);
+    return (((uint32_t)py << 16) | (uint32_t)px) + (uint32_t)sm.cell[base + offtab[key & 15u]].z;
+}
+
+// Alg. 2 at level l for one pixel, NearestSeed straight from the hash.
+__device__ __forceinline__ uint32_t direct_candidate(const StylizeArgs& a, const uint32_t* __restrict__ gtf, int px,
+                                                     int py, int l, uint32_t c_l) {
+    const int bx = px >> l, by = py >> l;
+    uint32_t best = 0xFFFFFFFFu;
+    int qx = 0, qy = 0;
+#pragma unroll
+    for (int x = -1; x <= 1; ++x)
+#pragma unroll
+        for (int y = -1; y <= 1; ++y) {
+            int cx, cy;
+            cell_seed(bx + x, by + y, l, c_l, a.zero_jitter != 0, cx, cy);
+            const int dx = cx - px, dy = cy - py;
+            const uint32_t key = 16u * (uint32_t)(dx * dx + dy * dy) + (uint32_t)(3 * (x + 1) + (y + 1));
+            if (key < best) { best = key; qx = cx; qy = cy; }
+        }
+    qx = min(max(qx, 0), a.wt - 1);
+    qy = min(max(qy, 0), a.ht - 1);
+    const uint32_t u = __ldg(a.lut + (__ldg(gtf + (uint32_t)(qy * a.wt + qx)) & 0xFFFFu));
+    const int sx = (int)(u & 0xFFFFu) + (px - qx);
+    const int sy = (int)(u >> 16) + (py - qy);
+    return (uint32_t)(sy * 65536 + sx);
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_constant__ StylizeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
 
-    const int tiles_x = (a.wt + TW - 1) / TW;
-    const int tile = blockIdx.x;
-    const int frame = blockIdx.y;
-    const int x0 = (tile % tiles_x) * TW;
-    const int y0 = a.row_begin + (tile / tiles_x) * TH;
+    const int x0 = blockIdx.x * TW;
+    const int y0 = a.row_begin + blockIdx.y * TH;
+    const int frame = blockIdx.z;
     const int64_t fpx = (int64_t)a.wt * a.ht;
     const uint32_t* __restrict__ gtf = reinterpret_cast<const uint32_t*>(a.gt) + fpx * frame;
     const uint32_t* __restrict__ gs = reinterpret_cast<const uint32_t*>(a.gs);
     const uint32_t seed = a.frame_seed(frame);
+    const uint32_t wt = (uint32_t)a.wt;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt_mask = (1u << lane) - 1u;
     const int rx0 = lane * 4;               // this thread's 4-pixel group column
-    const int ryA = warp, ryB = warp + 8;   // and its two rows
     const bool colok = x0 + rx0 < a.wt;     // wt % 4 == 0: a group is all in or all out
-    const bool okA = colok && (y0 + ryA) < a.row_end;
-    const bool okB = colok && (y0 + ryB) < a.row_end;
+    const int rows_here = min(TH, a.row_end - y0);
     const int L = a.L;
+    // tile row of this warp's j-th row, and whether its group exists
+    auto row_of = [&](int j) { return warp + NW * j; };
+    auto ok_of = [&](int j) { return colok && row_of(j) < rows_here; };
 
-    if (threadIdx.x < SB_MAX_LEVELS_DEV + 2) sm.qn[threadIdx.x] = 0;
-
-    // ---- load the G_T tile (streamed once from HBM) ----
-    uint4 gA = make_uint4(0, 0, 0, 0), gB = gA;
-    {
-        const uint64_t pol = policy_evict_first();
-        if (okA) gA = ld_stream_u4(gtf + (int64_t)(y0 + ryA) * a.wt + x0 + rx0, pol);
-        if (okB) gB = ld_stream_u4(gtf + (int64_t)(y0 + ryB) * a.wt + x0 + rx0, pol);
-    }
-    *reinterpret_cast<uint4*>(&sm.gt[ryA * TW + rx0]) = gA;
-    *reinterpret_cast<uint4*>(&sm.gt[ryB * TW + rx0]) = gB;
-
-    // ---- tables of levels L, L-1 and (when h >= 4 there) L-2, built together ----
+    // ---- tables of the levels among L, L-1, L-2 with h >= 4: the only CTA barrier ----
+    const bool t0 = L >= 2, t1 = L - 1 >= 2, t2 = L - 2 >= 2;
     const CellGrid gL = cell_grid(x0, y0, L, 0);
-    const int ncL = gL.ncx * gL.ncy;
+    const int ncL = t0 ? gL.ncx * gL.ncy : 0;
     const CellGrid gL1 = cell_grid(x0, y0, L - 1, ncL);
-    const int ncL1 = L >= 2 ? gL1.ncx * gL1.ncy : 0;
-    const bool pre2 = L >= 4;
+    const int ncL1 = t1 ? gL1.ncx * gL1.ncy : 0;
     const CellGrid gL2 = cell_grid(x0, y0, L - 2, ncL + ncL1);
-    const int ncL2 = pre2 ? gL2.ncx * gL2.ncy : 0;
+    const int ncL2 = t2 ? gL2.ncx * gL2.ncy : 0;
     write_offtab(sm.offtab[0], gL.ncy);
     write_offtab(sm.offtab[1], gL1.ncy);
     write_offtab(sm.offtab[2], gL2.ncy);
-    {
-        const uint32_t cL = level_salt(seed, L), cL1 = level_salt(seed, L - 1), cL2 = level_salt(seed, L - 2);
-        for (int c = threadIdx.x; c < ncL + ncL1 + ncL2; c += NT) {
-            if (c < ncL) build_one(sm, a, gtf, x0, y0, L, cL, gL, c);
-            else if (c < ncL + ncL1) build_one(sm, a, gtf, x0, y0, L - 1, cL1, gL1, c - ncL);
-            else build_one(sm, a, gtf, x0, y0, L - 2, cL2, gL2, c - ncL - ncL1);
-        }
+    for (int c = threadIdx.x; c < ncL + ncL1 + ncL2; c += NT) {
+        const bool s0 = c < ncL, s1 = c < ncL + ncL1;
+        CellGrid g;
+        g.cx0 = s0 ? gL.cx0 : (s1 ? gL1.cx0 : gL2.cx0);
+        g.cy0 = s0 ? gL.cy0 : (s1 ? gL1.cy0 : gL2.cy0);
+        g.ncy = s0 ? gL.ncy : (s1 ? gL1.ncy : gL2.ncy);
+        g.off = s0 ? 0 : (s1 ? ncL : ncL + ncL1);
+        const int l = s0 ? L : (s1 ? L - 1 : L - 2);
+        build_one(sm, a, gtf, x0, y0, l, level_salt(seed, l), g, c - g.off);
     }
     __syncthreads();
+    // From here on a warp only touches its own rows: no further CTA barrier.
 
-    int l;          // next level to process from the pixel queue q[cur]
-    int cur = 0;
-    int npx;        // number of entries in q[cur]
+    uint16_t* q = sm.wq[warp];
+    int n = 0;      // entries in the warp's pixel queue
+    int l;          // level of the pixel queue
+    const uint64_t pol = policy_evict_first();
     if (L >= 2) {
-        // ---- level L: every pixel, in 4-pixel groups ----
-        const bool group_next = (L - 1) >= 2;  // level L-1 also runs on groups
-        uint32_t rej[2] = {0, 0};
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const int ry = r ? ryB : ryA;
-            if (!(r ? okB : okA)) continue;
+        // ---- level L: every pixel, in 4-pixel groups; G_T streamed once from HBM ----
+        uint32_t rej = 0;  // 4 bits per row j
+#pragma unroll 2
+        for (int j = 0; j < RPW; ++j) {
+            if (!ok_of(j)) continue;
+            const int ry = row_of(j);
+            const uint4 gp4 = ld_stream_u4(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + rx0), pol);
             uint32_t cand[4];
-            const uint32_t acc = group_eval(sm, a, gs, gL, sm.offtab[0], L, x0, y0, rx0, ry, r ? gB : gA, cand);
+            const uint32_t acc = group_eval(sm, a, gs, gL, sm.offtab[0], L, x0, y0, rx0, ry, gp4, cand);
             *reinterpret_cast<uint4*>(&sm.coord[ry * TW + rx0]) = make_uint4(cand[0], cand[1], cand[2], cand[3]);
             *reinterpret_cast<uint32_t*>(&sm.lvl[ry * TW + rx0]) = 0x01010101u * (uint32_t)L;
-            rej[r] = ~acc & 0xFu;
+            rej |= (~acc & 0xFu) << (4 * j);
         }
-        if (group_next) {
-            // queue the groups with a rejected pixel
-            const int n_mine = (rej[0] != 0) + (rej[1] != 0);
-            int pos = warp_reserve(&sm.qn[L], n_mine);
+        if (t1) {
+            // ---- level L-1 on the warp's groups that still have a rejected pixel ----
+            uint16_t* gl = sm.glist[warp];
+            int ng = 0;
 #pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                if (!rej[r]) continue;
-                const int gid = (r ? ryB : ryA) * NG + lane;
-                sm.gmask[gid] = (uint8_t)rej[r];
-                sm.q[0][pos++] = (uint16_t)gid;
+            for (int j = 0; j < RPW; ++j) {
+                const uint32_t m = (rej >> (4 * j)) & 0xFu;
+                const unsigned b = __ballot_sync(0xFFFFFFFFu, m != 0);
+                if (m) gl[ng + __popc(b & lt_mask)] = (uint16_t)(lane | (j << 5) | (m << 8));
+                ng += __popc(b);
             }
-            __syncthreads();
-            // ---- level L-1: the queued groups, one per thread ----
-            const int ng = sm.qn[L];
+            __syncwarp();
             const int l1 = L - 1;
-            for (int j0 = 0; j0 < ng; j0 += NT) {
-                const int j = j0 + threadIdx.x;
+            for (int k0 = 0; k0 < ng; k0 += 32) {
+                const int k = k0 + lane;
                 uint32_t still = 0;
-                int gid = 0;
-                if (j < ng) {
-                    gid = sm.q[0][j];
-                    const int ry = gid / NG, grx0 = (gid % NG) * 4;
-                    const uint32_t m = sm.gmask[gid];
-                    const uint4 gp4 = *reinterpret_cast<const uint4*>(&sm.gt[ry * TW + grx0]);
+                int pbase = 0;
+                if (k < ng) {
+                    const uint32_t e = gl[k];
+                    const int grx0 = (int)(e & 31u) * 4;
+                    const int ry = row_of((int)((e >> 5) & 7u));
+                    const uint32_t m = e >> 8;
+                    pbase = ry * TW + grx0;
+                    const uint4 gp4 = *reinterpret_cast<const uint4*>(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + grx0));
                     uint32_t cand[4];
                     const uint32_t acc = group_eval(sm, a, gs, gL1, sm.offtab[1], l1, x0, y0, grx0, ry, gp4, cand);
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         if ((m >> i) & (acc >> i) & 1u) {
-                            sm.coord[ry * TW + grx0 + i] = cand[i];
-                            sm.lvl[ry * TW + grx0 + i] = (uint8_t)l1;
+                            sm.coord[pbase + i] = cand[i];
+                            sm.lvl[pbase + i] = (uint8_t)l1;
                         }
                     }
                     still = m & ~acc;
                 }
-                int pos2 = warp_reserve(&sm.qn[l1], __popc(still));
-                const int pbase = (gid / NG) * TW + (gid % NG) * 4;
+                int tot;
+                int pos = n + warp_excl_scan(__popc(still), &tot);
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
-                    if ((still >> i) & 1u) sm.q[1][pos2++] = (uint16_t)(pbase + i);
+                    if ((still >> i) & 1u) q[pos++] = (uint16_t)(pbase + i);
+                n += tot;
             }
-            __syncthreads();
-            npx = sm.qn[l1];
-            cur = 1;
             l = L - 2;
         } else {
             // L == 2: the rejected pixels go straight to the per-pixel levels
-            int pos = warp_reserve(&sm.qn[L], __popc(rej[0]) + __popc(rej[1]));
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                const int ry = r ? ryB : ryA;
+            int tot;
+            int pos = warp_excl_scan(__popc(rej), &tot);
+            for (int j = 0; j < RPW; ++j) {
+                const int ry = row_of(j);
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
-                    if ((rej[r] >> i) & 1u) sm.q[0][pos++] = (uint16_t)(ry * TW + rx0 + i);
+                    if ((rej >> (4 * j + i)) & 1u) q[pos++] = (uint16_t)(ry * TW + rx0 + i);
             }
-            __syncthreads();
-            npx = sm.qn[L];
-            cur = 0;
+            n = tot;
             l = L - 1;
         }
     } else {
         // L == 1: every valid pixel starts in the pixel queue
-        const int n_mine = (okA ? 4 : 0) + (okB ? 4 : 0);
-        __syncthreads();  // qn initialised
-        int pos = warp_reserve(&sm.qn[2], n_mine);
-        for (int r = 0; r < 2; ++r) {
-            if (!(r ? okB : okA)) continue;
-            const int ry = r ? ryB : ryA;
-            for (int i = 0; i < 4; ++i) sm.q[0][pos++] = (uint16_t)(ry * TW + rx0 + i);
+        int mine = 0;
+        for (int j = 0; j < RPW; ++j) mine += ok_of(j) ? 4 : 0;
+        int tot;
+        int pos = warp_excl_scan(mine, &tot);
+        for (int j = 0; j < RPW; ++j) {
+            if (!ok_of(j)) continue;
+            for (int i = 0; i < 4; ++i) q[pos++] = (uint16_t)(row_of(j) * TW + rx0 + i);
         }
-        __syncthreads();
-        npx = sm.qn[2];
-        cur = 0;
+        n = tot;
         l = 1;
     }
+    __syncwarp();
 
-    // ---- finer levels over the compacted pixel queue ----
-    for (; l >= 1 && npx > 0; --l) {
-        CellGrid g;
-        bool table = true;
-        const int* offtab;
-        if (l == L) {
-            g = gL;  // L == 1
-            offtab = sm.offtab[0];
-        } else if (l == L - 1) {
-            g = gL1;  // L == 2
-            offtab = sm.offtab[1];
-        } else if (l == L - 2 && pre2) {
-            g = gL2;
-            offtab = sm.offtab[2];
-        } else {
-            g = cell_grid(x0, y0, l, 0);
-            offtab = sm.offtab[3];
-            table = npx * 5 >= g.ncx * g.ncy;
-            if (table) {
-                const uint32_t c_l = level_salt(seed, l);
-                for (int c = threadIdx.x; c < g.ncx * g.ncy; c += NT) build_one(sm, a, gtf, x0, y0, l, c_l, g, c);
-                write_offtab(sm.offtab[3], g.ncy);
-                __syncthreads();
-            }
-        }
+    // ---- finer levels over the warp's pixel queue, compacted in place ----
+    for (; l >= 1 && n > 0; --l) {
+        const bool table = (l == L - 2 && t2) || (l == L - 1 && t1) || (l == L && t0);
+        const CellGrid& g = (l == L) ? gL : ((l == L - 1) ? gL1 : gL2);
+        const int* offtab = sm.offtab[(l == L) ? 0 : ((l == L - 1) ? 1 : 2)];
         const uint32_t c_l = level_salt(seed, l);
-        for (int j0 = 0; j0 < npx; j0 += NT) {
-            const int j = j0 + threadIdx.x;
+        int nn = 0;
+        for (int k0 = 0; k0 < n; k0 += 32) {
+            const int k = k0 + lane;
             bool rej = false;
             int idx = 0;
-            if (j < npx) {
-                idx = sm.q[cur][j];
+            if (k < n) {
+                idx = q[k];
                 const int rx = idx & (TW - 1), ry = idx / TW;
-                const int px = x0 + rx, py = y0 + ry;
-                uint32_t cand;
-                if (table) {
-                    const int base = g.off + ((px >> l) - g.cx0) * g.ncy + ((py >> l) - g.cy0);
-                    const int R4x = 4 * rx, R4y = 4 * ry;
-                    uint32_t kk[3];
-#pragma unroll
-                    for (int x = -1; x <= 1; ++x) {
-                        uint32_t kx[3];
-#pragma unroll
-                        for (int y = -1; y <= 1; ++y) {
-                            const int2 s = *reinterpret_cast<const int2*>(&sm.cell[base + x * g.ncy + y]);
-                            const int dx4 = s.x - R4x, dy4 = s.y - R4y;
-                            kx[y + 1] = (uint32_t)(dx4 * dx4) + (uint32_t)(dy4 * dy4) + (uint32_t)(3 * (x + 1) + (y + 1));
-                        }
-                        kk[x + 1] = min3u(kx[0], kx[1], kx[2]);
-                    }
-                    const uint32_t key = min3u(kk[0], kk[1], kk[2]);
-                    cand = (((uint32_t)py << 16) | (uint32_t)px) + (uint32_t)sm.cell[base + offtab[key & 15u]].z;
-                } else {
-                    // direct NearestSeed from the hash (few pixels reach this level)
-                    const int bx = px >> l, by = py >> l;
-                    uint32_t best = 0xFFFFFFFFu;
-                    int qx = 0, qy = 0;
-#pragma unroll
-                    for (int x = -1; x <= 1; ++x)
-#pragma unroll
-                        for (int y = -1; y <= 1; ++y) {
-                            int cx, cy;
-                            cell_seed(bx + x, by + y, l, c_l, a.zero_jitter != 0, cx, cy);
-                            const int dx = cx - px, dy = cy - py;
-                            const uint32_t key = 16u * (uint32_t)(dx * dx + dy * dy) + (uint32_t)(3 * (x + 1) + (y + 1));
-                            if (key < best) { best = key; qx = cx; qy = cy; }
-                        }
-                    qx = min(max(qx, 0), a.wt - 1);
-                    qy = min(max(qy, 0), a.ht - 1);
-                    const uint32_t u = __ldg(a.lut + (__ldg(gtf + (uint32_t)(qy * a.wt + qx)) & 0xFFFFu));
-                    const int sx = (int)(u & 0xFFFFu) + (px - qx);
-                    const int sy = (int)(u >> 16) + (py - qy);
-                    cand = (uint32_t)(sy * 65536 + sx);
-                }
-                if (accept(a, gs, sm.gt[idx], cand)) {
+                const uint32_t cand = table ? table_candidate(sm, g, offtab, l, x0, y0, rx, ry)
+                                            : direct_candidate(a, gtf, x0 + rx, y0 + ry, l, c_l);
+                const uint32_t gp = __ldg(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + rx));
+                if (accept(a, gs, gp, cand)) {
                     sm.coord[idx] = cand;
                     sm.lvl[idx] = (uint8_t)l;
                 } else {
                     rej = true;
                 }
             }
-            const unsigned m = __ballot_sync(0xFFFFFFFFu, rej);
-            int base = 0;
-            if (lane == 0 && m) base = atomicAdd(&sm.qn[l - 1], __popc(m));
-            base = __shfl_sync(0xFFFFFFFFu, base, 0);
-            if (rej) sm.q[cur ^ 1][base + __popc(m & ((1u << lane) - 1u))] = (uint16_t)idx;
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, rej);  // all reads of this round are done
+            if (rej) q[nn + __popc(m & lt_mask)] = (uint16_t)idx;  // nn + rank <= k: in place
+            nn += __popc(m);
         }
-        __syncthreads();
-        npx = sm.qn[l - 1];
-        cur ^= 1;
+        __syncwarp();
+        n = nn;
     }
 
     // ---- level 0: the look-up fallback (reading R12) ----
     if (l == 0) {
-        for (int j = threadIdx.x; j < npx; j += NT) {
-            const int idx = sm.q[cur][j];
-            sm.coord[idx] = __ldg(a.lut + (sm.gt[idx] & 0xFFFFu));
+        for (int k = lane; k < n; k += 32) {
+            const int idx = q[k];
+            const int rx = idx & (TW - 1), ry = idx / TW;
+            const uint32_t gp = __ldg(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + rx));
+            sm.coord[idx] = __ldg(a.lut + (gp & 0xFFFFu));
             sm.lvl[idx] = 0;
         }
     }
-    __syncthreads();
+    __syncwarp();
 
     // ---- outputs: coords, levels, blit colours ----
     const uint32_t* __restrict__ cs = reinterpret_cast<const uint32_t*>(a.cs);
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        const int ry = r ? ryB : ryA;
-        if (!(r ? okB : okA)) continue;
-        const int64_t o = fpx * frame + (int64_t)(y0 + ry) * a.wt + x0 + rx0;
+    const uint32_t ws = (uint32_t)a.ws;
+#pragma unroll 2
+    for (int j = 0; j < RPW; ++j) {
+        if (!ok_of(j)) continue;
+        const int ry = row_of(j);
+        const int64_t o = fpx * frame + (int64_t)((y0 + ry) * wt + (uint32_t)(x0 + rx0));
         const uint4 cv = *reinterpret_cast<const uint4*>(&sm.coord[ry * TW + rx0]);
         if (a.coords) st_cs_u4(a.coords + o, cv);
         if (a.level) st_cs_u32(a.level + o, *reinterpret_cast<const uint32_t*>(&sm.lvl[ry * TW + rx0]));
         if (a.ct) {
             uint4 col;
-            const uint32_t ws = (uint32_t)a.ws;
             col.x = __ldg(cs + ((cv.x >> 16) * ws + (cv.x & 0xFFFFu)));
             col.y = __ldg(cs + ((cv.y >> 16) * ws + (cv.y & 0xFFFFu)));
             col.z = __ldg(cs + ((cv.z >> 16) * ws + (cv.z & 0xFFFFu)));
@@ -423,12 +399,12 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
 }
 
 cudaError_t launch_stylize_tiled(const StylizeArgs& a, int n_frames, cudaStream_t st, int* launches) {
-    static_assert(sizeof(Smem) <= 64 * 1024, "smem");
-    const int tiles = ((a.wt + TW - 1) / TW) * ((a.row_end - a.row_begin + TH - 1) / TH);
+    static_assert(sizeof(Smem) <= 48 * 1024, "smem");
     const size_t smem = sizeof(Smem);
     cudaError_t e = cudaFuncSetAttribute(stylize_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)tiles, (unsigned)n_frames);
+    dim3 grid((unsigned)((a.wt + TW - 1) / TW), (unsigned)((a.row_end - a.row_begin + TH - 1) / TH),
+              (unsigned)n_frames);
     stylize_tiled_kernel<<<grid, NT, smem, st>>>(a);
     *launches += 1;
     return cudaPeekAtLastError();
