@@ -18,11 +18,13 @@
 //   2. per pixel: the window is one chunk iff its 2r+1 row segments are and the centre column
 //      continues vertically -- then the vote is unanimous and C_T[p] = C_S[src(p)] (the chunk
 //      interior, where voting equals the blit): one gather;
-//   3. the other pixels go to a shared-memory queue, processed densely one pixel per thread,
+//   3. the other pixels go to shared-memory queues, processed densely one pixel per thread,
 //      window row by window row: the row-link bits split a row into runs of positions that
-//      vote for the same source pixel, and each run costs one gather weighted by its length
-//      (typically 1-2 runs per row instead of 2r+1 gathers).  Sums are SWAR (two 16-bit
-//      lanes per register; (2r+1)^2 * 255 < 2^16 for r <= 7); division by (2r+1)^2.
+//      vote for the same source pixel, and each run costs one gather weighted by its length.
+//      Pixels whose rows have at most two runs (most) take a branch-free two-gather row
+//      step; the others a run loop, in their own queue so warps do not diverge.  Sums are
+//      SWAR (two 16-bit lanes per register; (2r+1)^2 * 255 < 2^16 for r <= 7); division by
+//      (2r+1)^2.
 // Border tiles: every pixel takes the general per-position path with target clipping and
 // source bounds tests on packed coordinates (x | y<<16; for W, H <= 32767 and |d| <= 2r the
 // packed sum src(q) + (p-q) never carries between fields and any position left of / above
@@ -57,6 +59,17 @@ __device__ __forceinline__ uint32_t finish_const(uint32_t lo, uint32_t hi) {
     return c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
 }
 
+// Predicated gather: returns 0 without touching memory when !pred (keeps L1 traffic to the
+// gathers that matter, without a branch).
+__device__ __forceinline__ uint32_t ldg_if(const uint32_t* p, bool pred) {
+    uint32_t v = 0;
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.u32 %0, [%1];\n\t}"
+        : "+r"(v)
+        : "l"(p), "r"((uint32_t)pred));
+    return v;
+}
+
 __device__ __forceinline__ void swar_add(uint32_t c, uint32_t& lo, uint32_t& hi) {
     lo += c & 0x00FF00FFu;
     hi += __byte_perm(c, 0u, 0x7371);  // bytes 1 and 3 into 16-bit lanes
@@ -71,10 +84,11 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 8 : 2)) vote_kernel(const VoteAr
     constexpr int SWP = OFF + TW + OFF;       // 16-byte aligned rows
     __shared__ __align__(16) uint32_t sc[SH][SWP];
     __shared__ uint8_t seg[SH][NG];        // nibble: which of the group's 4 row segments are one chunk
+    __shared__ uint8_t seg3[SH][NG];       // nibble: which of them have three or more runs
     __shared__ uint32_t hl[SH][6];         // row link bits: bit x+32 <=> position x+1 continues x
     __shared__ __align__(16) uint32_t outc[TH][TW];
-    __shared__ uint16_t queue[TH * TW];
-    __shared__ int qn;
+    __shared__ uint16_t queue[TH * TW];    // two-run pixels from the front, others from the back
+    __shared__ int qn, qn3;
 
     const int tiles_x = (a.wt + TW - 1) / TW;
     const int x0 = (blockIdx.x % tiles_x) * TW;
@@ -85,7 +99,7 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 8 : 2)) vote_kernel(const VoteAr
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t ws = (uint32_t)a.ws, hs = (uint32_t)a.hs;
 
-    if (threadIdx.x == 0) qn = 0;
+    if (threadIdx.x == 0) qn = qn3 = 0;
     // ---- stage coords (tile + halo), outside the target -> kOutside; test the fast-tile margin
     bool fast_mine = true;
     auto stage = [&](int yy, int x, uint32_t v, bool in) {  // x: tile column (-R .. TW-1+R)
@@ -175,6 +189,10 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 8 : 2)) vote_kernel(const VoteAr
 #pragma unroll
                 for (int k = 0; k < 4; ++k) nib |= (uint32_t)(((link >> k) & win) == win) << k;
                 seg[yy][gg] = (uint8_t)nib;
+                uint32_t nib3 = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) nib3 |= (uint32_t)(__popc(~(link >> k) & win) >= 2) << k;
+                seg3[yy][gg] = (uint8_t)nib3;
                 // assemble the row's link words (a warp holds one staged row: lane == group)
                 uint32_t wv = ((link >> R) & 0xFu) << (4 * (gg & 7));
                 wv |= __shfl_xor_sync(0xFFFFFFFFu, wv, 1);
@@ -186,19 +204,21 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 8 : 2)) vote_kernel(const VoteAr
             }
             __syncthreads();
         }
-        // ---- 2. per pixel: unanimous window -> blit, else queue
-        int my_n = 0;
-        uint32_t my_mask = 0;  // bit 4*rr + k: queued
+        // ---- 2. per pixel: unanimous window -> blit; else queue it, apart if a window row has
+        //      three or more runs
+        int my_n = 0, my_n3 = 0;
+        uint32_t my_mask = 0, my_mask3 = 0;  // bit 4*rr + k: queued
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
             const int ry = warp + 8 * rr;
             if (y0 + ry >= a.row_end || x0 + 4 * g >= a.wt) continue;
             const uint4 c4 = *reinterpret_cast<const uint4*>(&sc[ry + R][OFF + 4 * g]);
             const uint32_t cp[4] = {c4.x, c4.y, c4.z, c4.w};
-            uint32_t uni = 0xFu;
+            uint32_t uni = 0xFu, cx3 = 0;
 #pragma unroll
             for (int j = -R; j <= R; ++j) {
                 uint32_t m = seg[ry + R + j][g];
+                cx3 |= seg3[ry + R + j][g];
                 const uint4 v4 = *reinterpret_cast<const uint4*>(&sc[ry + R + j][OFF + 4 * g]);
                 const uint32_t vv[4] = {v4.x, v4.y, v4.z, v4.w};
                 const uint32_t sh = (uint32_t)j * ws;
@@ -210,34 +230,76 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 8 : 2)) vote_kernel(const VoteAr
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 o[k] = 0;
-                if ((uni >> k) & 1u) o[k] = __ldg(cs + cp[k]);
-                else { my_mask |= 1u << (4 * rr + k); ++my_n; }
+                if ((uni >> k) & 1u) {
+                    o[k] = __ldg(cs + cp[k]);
+                } else if ((cx3 >> k) & 1u) {
+                    my_mask3 |= 1u << (4 * rr + k);
+                    ++my_n3;
+                } else {
+                    my_mask |= 1u << (4 * rr + k);
+                    ++my_n;
+                }
             }
             *reinterpret_cast<uint4*>(&outc[ry][4 * g]) = make_uint4(o[0], o[1], o[2], o[3]);
         }
-        int incl = my_n;
+        {
+            int incl = my_n, incl3 = my_n3;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= o) incl += v;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                const int v3 = __shfl_up_sync(0xFFFFFFFFu, incl3, o);
+                if (lane >= o) { incl += v; incl3 += v3; }
+            }
+            const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+            const int total3 = __shfl_sync(0xFFFFFFFFu, incl3, 31);
+            int base = 0, base3 = 0;
+            if (lane == 31) {
+                if (total) base = atomicAdd(&qn, total);
+                if (total3) base3 = atomicAdd(&qn3, total3);
+            }
+            base = __shfl_sync(0xFFFFFFFFu, base, 31) + incl - my_n;
+            base3 = __shfl_sync(0xFFFFFFFFu, base3, 31) + incl3 - my_n3;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const uint16_t id = (uint16_t)((warp + 8 * (b >> 2)) * TW + 4 * g + (b & 3));
+                if (my_mask & (1u << b)) queue[base++] = id;
+                if (my_mask3 & (1u << b)) queue[TH * TW - 1 - base3++] = id;
+            }
         }
-        const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        int base = 0;
-        if (lane == 31 && total) base = atomicAdd(&qn, total);
-        base = __shfl_sync(0xFFFFFFFFu, base, 31) + incl - my_n;
-#pragma unroll
-        for (int b = 0; b < 8; ++b)
-            if (my_mask & (1u << b)) queue[base++] = (uint16_t)((warp + 8 * (b >> 2)) * TW + 4 * g + (b & 3));
         __syncthreads();
-        // ---- 3. dense per-pixel voting by runs: within a window row, consecutive positions
-        //      whose offsets agree (the row-link bits) vote for the same source pixel, so each
-        //      run costs one gather weighted by its length.
+        constexpr uint32_t W = 2 * R + 1;
+        // ---- 3a. two-run pixels, densely and branch-free: in each window row the link bits
+        //      split the 2r+1 positions into at most two runs of positions that vote for the
+        //      same source pixel; each run costs one gather weighted by its length.
         const int n = qn;
         for (int j = threadIdx.x; j < n; j += NT) {
             const int idx = queue[j];
             const int ry = idx / TW, x = idx - ry * TW;
             uint32_t lo = 0, hi = 0;
-            constexpr uint32_t W = 2 * R + 1;
+#pragma unroll
+            for (int dy = -R; dy <= R; ++dy) {
+                const int yy = ry + R + dy;
+                const uint32_t b = (uint32_t)(x - R + 32);
+                const uint32_t bits = __funnelshift_r(hl[yy][b >> 5], hl[yy][(b >> 5) + 1], b & 31u);
+                const uint32_t m = ~bits & ((1u << (2 * R)) - 1u);  // at most one run end
+                const uint32_t c1 = m ? (uint32_t)__ffs(m) : W;      // length of run 1
+                const uint32_t h2 = c1 < W ? c1 : 0u;                // head of run 2 (or any)
+                const uint32_t* row = &sc[yy][OFF + x - R];
+                const uint32_t shy = (uint32_t)dy * ws;
+                const uint32_t col1 = __ldg(cs + (row[0] - shy + (uint32_t)R));
+                const uint32_t c2 = W - c1;
+                const uint32_t col2 = ldg_if(cs + (row[h2] - shy - (h2 - (uint32_t)R)), c2 != 0);
+                lo += (col1 & 0x00FF00FFu) * c1 + (col2 & 0x00FF00FFu) * c2;
+                hi += __byte_perm(col1, 0u, 0x7371) * c1 + __byte_perm(col2, 0u, 0x7371) * c2;
+            }
+            outc[ry][x] = finish_const<W * W>(lo, hi);
+        }
+        // ---- 3b. pixels with a row of three or more runs: the general run loop
+        const int n3 = qn3;
+        for (int j = threadIdx.x; j < n3; j += NT) {
+            const int idx = queue[TH * TW - 1 - j];
+            const int ry = idx / TW, x = idx - ry * TW;
+            uint32_t lo = 0, hi = 0;
 #pragma unroll
             for (int dy = -R; dy <= R; ++dy) {
                 const int yy = ry + R + dy;
