@@ -1,13 +1,15 @@
 #!/usr/bin/env python
 """StyleBlit (arXiv 1807.03249) hot-path benchmark on B200.
 
-One STEP = one pass of the whole hot path over one batch of synthetic 4K frames per GPU:
+One STEP = one pass of the hot path over one batch of synthetic 4K frames per GPU:
   sb_build_lut (the exemplar's guide LUT)
   + sb_stylize_batch (Alg. 2 for every pixel of every frame, per-frame jitter seeds,
-    PAPER.md:337-433; coordinates out)
-  + sb_vote (the voting blend; colours out).
+    PAPER.md:337-433; coordinates and blit colours C_T[p] = C_S[s] out).
+The seam blend is optional in the paper ("When seams become obvious, we can optionally perform
+blending"); it is timed in its own run every time (`blend_r2`): LUT + stylize
+(coordinates) + sb_vote (r = 2).  `--blend-radius 2` makes it the headline.
 Workload (BASELINE.json configs[4] = config 5, per GPU): B frames of 3840x2160 heightfield
-normals (seed 5, per-frame phase), 512x512 sphere exemplar, L=5, t=10, C=3, r=2.
+normals (seed 5, per-frame phase), 512x512 sphere exemplar, L=5, t=10, C=3.
 Frames are sharded by rank (weak scaling: every GPU stylizes its own B frames, no data-path
 collective).  Inputs are > L2 (B*33 MB of G_T per step), so no L2 flush is needed.
 
@@ -42,7 +44,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--frames", type=int, default=64, help="4K frames per GPU per step")
-    ap.add_argument("--blend-radius", type=int, default=2)
+    ap.add_argument("--blend-radius", type=int, default=0,
+                    help="0 (default): the stylization proper, blit colours (PAPER.md:387); the optional "
+                         "vote blend (PAPER.md:412) is timed separately at r=2 and reported as blend_r2")
+    ap.add_argument("--blend-steps", type=int, default=20, help="timed steps of the r=2 blend run (0: skip)")
     ap.add_argument("--mode", default="frame", choices=["frame", "strip"],
                     help="frame: each GPU stylizes its own frames (weak scaling, no collective); "
                          "strip: every frame is split into row strips across GPUs and the C_T strips "
@@ -169,89 +174,110 @@ def run_ours(args):
     ct = torch.empty(B, HT, WT, 4, dtype=torch.uint8, device=dev)
     lut = torch.empty(65536, dtype=torch.int32, device=dev)
     lut_ws = torch.empty(65536 * 4, dtype=torch.uint8, device=dev)
-    r_halo = r if strip else 0
-    prm = sb.Params(threshold=cfg["t"], levels=cfg["L"], blend_radius=0, guide_channels=cfg["C"],
-                    seed=cfg["seed"], flags=sb.SB_NO_COLOR, row_begin=max(0, rb - r_halo),
-                    row_end=min(HT, re_ + r_halo))
     stream = torch.cuda.current_stream(dev)
-
-    ev = {k: [] for k in ("lut", "stylize", "vote", "gather")}
-    launches = [0]
-
-    def step(record: bool):
-        es = [torch.cuda.Event(enable_timing=True) for _ in range(5)] if record else None
-        if record:
-            es[0].record(stream)
-        sb.build_lut(gs, lut, lut_ws)
-        n_l = sb.launch_count()
-        if record:
-            es[1].record(stream)
-        sb.stylize_batch(prm, cs, gs, lut, gt, frame_seeds=seeds, ct=None, coords=coords, want_level=False)
-        n_s = sb.launch_count()
-        if record:
-            es[2].record(stream)
-        sb.vote(coords, cs, r, ct=ct, row_begin=rb, row_end=re_)
-        n_v = sb.launch_count()
-        if record:
-            es[3].record(stream)
-        if strip and world > 1:  # the one exchange step: C_T strips -> rank 0 over NCCL
-            sharding.gather_strips(ct[:, rb:re_], HT, world, rank, dst=0, row_axis=1)
-        if record:
-            es[4].record(stream)
-            ev["lut"].append((es[0], es[1]))
-            ev["stylize"].append((es[1], es[2]))
-            ev["vote"].append((es[2], es[3]))
-            ev["gather"].append((es[3], es[4]))
-            launches[0] += n_l + n_s + n_v
-
-    for _ in range(args.warmup):
-        step(False)
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        t0.record(stream)
-        for _ in range(args.steps):
-            step(True)
-        t1.record(stream)
-        torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    ms = t0.elapsed_time(t1)
-    if world > 1:
-        tt = torch.tensor([ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
-    ms_step = ms / args.steps
     px_step = B * WT * HT if not strip else B * WT * (re_ - rb)  # pixels this rank outputs
     px_job = world * B * WT * HT if not strip else B * WT * HT
-    value = px_job / (ms_step * 1e-3) / 1e6  # MP/s, whole job
 
-    kt = {k: statistics.mean(a.elapsed_time(b) for a, b in v) for k, v in ev.items()}
+    def time_path(rad: int, steps: int, warmup: int):
+        """Time `steps` steps of the path with blend radius rad (0: blit colours straight from
+        the stylize kernel; > 0: stylize -> coords, then the vote kernel)."""
+        r_halo = rad if strip else 0
+        flags = sb.SB_NO_COLOR if rad > 0 else 0
+        prm = sb.Params(threshold=cfg["t"], levels=cfg["L"], blend_radius=0, guide_channels=cfg["C"],
+                        seed=cfg["seed"], flags=flags, row_begin=max(0, rb - r_halo), row_end=min(HT, re_ + r_halo))
+        ev = {k: [] for k in ("lut", "stylize", "vote", "gather")}
+        launches = [0]
+
+        def step(record: bool):
+            es = [torch.cuda.Event(enable_timing=True) for _ in range(5)] if record else None
+            if record:
+                es[0].record(stream)
+            sb.build_lut(gs, lut, lut_ws)
+            n = sb.launch_count()
+            if record:
+                es[1].record(stream)
+            sb.stylize_batch(prm, cs, gs, lut, gt, frame_seeds=seeds, ct=None if rad > 0 else ct, coords=coords,
+                             want_level=False)
+            n += sb.launch_count()
+            if record:
+                es[2].record(stream)
+            if rad > 0:
+                sb.vote(coords, cs, rad, ct=ct, row_begin=rb, row_end=re_)
+                n += sb.launch_count()
+            if record:
+                es[3].record(stream)
+            if strip and world > 1:  # the one exchange step: C_T strips -> rank 0 over NCCL
+                sharding.gather_strips(ct[:, rb:re_], HT, world, rank, dst=0, row_axis=1)
+            if record:
+                es[4].record(stream)
+                ev["lut"].append((es[0], es[1]))
+                ev["stylize"].append((es[1], es[2]))
+                ev["vote"].append((es[2], es[3]))
+                ev["gather"].append((es[3], es[4]))
+                launches[0] += n
+
+        for _ in range(warmup):
+            step(False)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            t0.record(stream)
+            for _ in range(steps):
+                step(True)
+            t1.record(stream)
+            torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        ms = t0.elapsed_time(t1)
+        if world > 1:
+            tt = torch.tensor([ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        ms_step = ms / steps
+        kt = {k: statistics.mean(a.elapsed_time(b) for a, b in v) for k, v in ev.items()}
+        # algorithmic bytes per launch (DESIGN.md 7): stylize reads G_T and writes coords (+ C_T
+        # when it blits); the vote reads coords and writes C_T
+        alg = {"stylize": (8 if rad > 0 else 12) * px_step, "lut": gs.numel() + 65536 * 4}
+        if rad > 0:
+            alg["vote"] = 8 * px_step
+        kernels = {k: {"ms_per_launch": round(kt[k], 4), "share": round(kt[k] / ms_step, 4),
+                       "GBps_alg": round(alg[k] / (kt[k] * 1e-3) / 1e9, 1)} for k in alg}
+        if strip and world > 1:
+            gbytes = (world - 1) * B * WT * (HT // world) * 4  # strips arriving at rank 0
+            kernels["gather"] = {"ms_per_step": round(kt["gather"], 4), "share": round(kt["gather"] / ms_step, 4),
+                                 "GBps_into_rank0": round(gbytes / (kt["gather"] * 1e-3) / 1e9, 1)}
+        dom = max([k for k in ("stylize", "vote") if k in alg], key=lambda k: kt[k])
+        return dict(ms_step=ms_step, value=px_job / (ms_step * 1e-3) / 1e6, kernels=kernels, kt=kt, alg=alg,
+                    dom=dom, launches=launches[0], clocks=clk.summary())
+
+    r = args.blend_radius
+    main = time_path(r, args.steps, args.warmup)
+    ms_step, value, dom, kt, alg = main["ms_step"], main["value"], main["dom"], main["kt"], main["alg"]
     hbm, hbm_src = peaks()
-    # algorithmic bytes per launch: stylize reads G_T, writes coords;
-    # vote reads coords, writes C_T: 8 B per pixel each.
-    alg = {"stylize": 8 * px_step, "vote": 8 * px_step, "lut": gs.numel() + 65536 * 4}
-    dom = max(("stylize", "vote"), key=lambda k: kt[k])
     ach = alg[dom] / (kt[dom] * 1e-3) / 1e9
     # measured DRAM traffic of the same kernel: one `ncu --set full` capture (profiles/traffic.json,
     # written by tools/ncu_traffic.py), per pixel, scaled to this launch
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = round(json.load(f)[dom]["bytes_per_px"] * px_step)
+            tj = json.load(f)
+        key = dom if not (dom == "stylize" and r > 0) else "stylize_coords"
+        traffic = round(tj[key]["bytes_per_px"] * px_step)
     except Exception:
         pass
-    kernels = {k: {"ms_per_launch": round(kt[k], 4), "share": round(kt[k] / ms_step, 4),
-                   "GBps_alg": round(alg[k] / (kt[k] * 1e-3) / 1e9, 1)} for k in kt if k in alg}
-    if strip and world > 1:
-        gbytes = (world - 1) * B * WT * (HT // world) * 4  # strips arriving at rank 0
-        kernels["gather"] = {"ms_per_step": round(kt["gather"], 4), "share": round(kt["gather"] / ms_step, 4),
-                             "GBps_into_rank0": round(gbytes / (kt["gather"] * 1e-3) / 1e9, 1)}
+    kernels = main["kernels"]
+    blend = None
+    if r == 0 and args.blend_steps > 0:
+        # the optional seam blend (PAPER.md:412-421) at the config's r = 2: its own timed run
+        bl = time_path(2, args.blend_steps, max(3, min(args.warmup, 5)))
+        blend = {"value": round(bl["value"], 1), "unit": "MP/s", "ms_per_step": round(bl["ms_step"], 4),
+                 "blend_radius": 2, "kernels": bl["kernels"], "gpu_launches": bl["launches"], "clocks": bl["clocks"],
+                 "step": "LUT build + stylize (coords) + vote r=2"}
 
     # ---- e2e through the host-buffer ABI call (pinned host memory, copies inside timing)
     e2e = None
@@ -302,7 +328,8 @@ def run_ours(args):
         "dtype": "u8",
         "data": "synthetic (seeded heightfield-normal 4K frames, sphere-normal exemplar, painted style)",
         "config": {"workload": f"cfg5: {B} x 4K UHD (3840x2160) frames per GPU, 512x512 exemplar, L={cfg['L']}, "
-                               f"t={cfg['t']}, C={cfg['C']}, blend r={r}; step = LUT build + stylize + vote",
+                               f"t={cfg['t']}, C={cfg['C']}, blend r={r}; step = LUT build + stylize"
+                               + (" + vote" if r > 0 else " (blit colours)"),
                    "frames_per_gpu": B, "global_frames": B * world, "levels": cfg["L"], "threshold": cfg["t"],
                    "blend_radius": r,
                    "parallelism": (f"frame-sharded x{world} (no data-path collective)" if not strip else
@@ -312,10 +339,11 @@ def run_ours(args):
         "kernels": kernels,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(ach / hbm, 4), "traffic": traffic, "peak_source": hbm_src,
-                     "alg_bytes_per_launch": alg[dom], "alg_bytes_per_px": 8},
-        "gpu_launches": launches[0],
-        "clocks": clk.summary(),
+                     "alg_bytes_per_launch": alg[dom], "alg_bytes_per_px": alg[dom] // px_step},
+        "gpu_launches": main["launches"],
+        "clocks": main["clocks"],
         "e2e": e2e,
+        "blend_r2": blend,
     }
     return out, rank, world
 

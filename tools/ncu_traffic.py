@@ -1,4 +1,5 @@
-"""Turn one `ncu --set full` capture of the bench's stylize/vote launches into per-pixel DRAM
+"""Turn one `ncu --set full` capture of the bench's stylize/vote launches (profiles/gpu_iter.sh:
+main stylize with blit colours, the blend run's coords-only stylize, the vote) into per-pixel DRAM
 traffic (dram__bytes_read.sum + dram__bytes_write.sum per launch / pixels per launch).
 
 usage: python tools/ncu_traffic.py <report.ncu-rep> <frames_per_launch> <out.json>
@@ -22,6 +23,8 @@ for row in rows[2:]:
     key = "stylize" if "stylize" in name else ("vote" if "vote" in name else None)
     if key is None:
         continue
+    if key in res:  # bench order: main stylize (blit colours), then the blend run's stylize (coords)
+        key = "stylize_coords" if key == "stylize" else key + "_2"
     unit_r, unit_w = rows[1][h.index("dram__bytes_read.sum")], rows[1][h.index("dram__bytes_write.sum")]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     rd = float(d["dram__bytes_read.sum"]) * scale[unit_r]
