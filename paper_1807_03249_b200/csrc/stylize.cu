@@ -47,7 +47,7 @@ struct Smem {
     uint8_t lvl[TP];              // result levels
     uint16_t wq[NW][WPX];         // per-warp pixel queue (compacted in place)
     uint16_t glist[NW][RPW * NG]; // per-warp list of groups with a rejected pixel
-    int4 cell[MAXCELLS];          // seed/offset tables, row-major per level (ci*ncy + cj)
+    int4 cell[MAXCELLS];          // seed/offset tables, row-major per level (cj*ncx + ci)
     int offtab[3][16];            // winner offsets per table slot (L, L-1, L-2)
 };
 
@@ -67,9 +67,9 @@ __device__ __forceinline__ CellGrid cell_grid(int x0, int y0, int l, int off) {
 
 __device__ __forceinline__ void build_one(Smem& sm, const StylizeArgs& a, const uint32_t* __restrict__ gtf, int x0,
                                           int y0, int l, uint32_t c_l, const CellGrid& g, int c) {
-    // c < ncx*ncy <= 1000: (c + 0.5) / ncy is >= 0.04 away from an integer, float-exact floor
-    const int ci = (int)(((float)c + 0.5f) * __frcp_rn((float)g.ncy));
-    const int cj = c - ci * g.ncy;
+    // c < ncx*ncy <= 1000: (c + 0.5) / ncx is >= 0.007 away from an integer, float-exact floor
+    const int cj = (int)(((float)c + 0.5f) * __frcp_rn((float)g.ncx));
+    const int ci = c - cj * g.ncx;
     int sx, sy;
     cell_seed(g.cx0 + ci, g.cy0 + cj, l, c_l, a.zero_jitter != 0, sx, sy);
     const int qx = min(max(sx, 0), a.wt - 1);
@@ -80,9 +80,11 @@ __device__ __forceinline__ void build_one(Smem& sm, const StylizeArgs& a, const 
     sm.cell[g.off + c] = make_int4(4 * (sx - x0), 4 * (sy - y0), dpack, 0);
 }
 
-// Winner-offset table of a level: cell index offset of loop-order candidate i (0..8).
-__device__ __forceinline__ void write_offtab(int* tab, int ncy) {
-    if (threadIdx.x < 9) tab[threadIdx.x] = (int)(threadIdx.x / 3 - 1) * ncy + (int)(threadIdx.x % 3) - 1;
+// Winner-offset table of a level: cell index offset of loop-order candidate i (0..8), i.e.
+// of cell (x, y) = (i/3 - 1, i%3 - 1) in the row-major table.  (Row-major so that lanes of a
+// warp, which sit in different cell columns, read different shared-memory banks.)
+__device__ __forceinline__ void write_offtab(int* tab, int ncx) {
+    if (threadIdx.x < 9) tab[threadIdx.x] = (int)(threadIdx.x / 3) - 1 + ((int)(threadIdx.x % 3) - 1) * ncx;
 }
 
 __device__ __forceinline__ uint32_t min3u(uint32_t a, uint32_t b, uint32_t c) { return min(min(a, b), c); }
@@ -118,14 +120,14 @@ __device__ __forceinline__ uint32_t group_eval(const Smem& sm, const StylizeArgs
                                                const CellGrid& g, const int* offtab, int l, int x0, int y0, int rx0,
                                                int ry, uint4 gp4, uint32_t cand[4]) {
     const int py = y0 + ry, px0 = x0 + rx0;
-    const int base = g.off + ((px0 >> l) - g.cx0) * g.ncy + ((py >> l) - g.cy0);
+    const int base = g.off + ((py >> l) - g.cy0) * g.ncx + ((px0 >> l) - g.cx0);
     uint32_t k0 = 0xFFFFFFFFu, k1 = k0, k2 = k0, k3 = k0;
     const int R4x = 4 * rx0, R4y = 4 * ry;
 #pragma unroll
     for (int x = -1; x <= 1; ++x) {
 #pragma unroll
         for (int y = -1; y <= 1; ++y) {
-            const int2 s = *reinterpret_cast<const int2*>(&sm.cell[base + x * g.ncy + y]);
+            const int2 s = *reinterpret_cast<const int2*>(&sm.cell[base + x + y * g.ncx]);
             const int dy4 = s.y - R4y;
             const int dx4 = s.x - R4x;
             const uint32_t A = (uint32_t)(dx4 * dx4) + (uint32_t)(dy4 * dy4) + (uint32_t)(3 * (x + 1) + (y + 1));
@@ -152,7 +154,7 @@ __device__ __forceinline__ uint32_t group_eval(const Smem& sm, const StylizeArgs
 __device__ __forceinline__ uint32_t table_candidate(const Smem& sm, const CellGrid& g, const int* offtab, int l,
                                                     int x0, int y0, int rx, int ry) {
     const int px = x0 + rx, py = y0 + ry;
-    const int base = g.off + ((px >> l) - g.cx0) * g.ncy + ((py >> l) - g.cy0);
+    const int base = g.off + ((py >> l) - g.cy0) * g.ncx + ((px >> l) - g.cx0);
     const int R4x = 4 * rx, R4y = 4 * ry;
     uint32_t kk[3];
 #pragma unroll
@@ -160,7 +162,7 @@ __device__ __forceinline__ uint32_t table_candidate(const Smem& sm, const CellGr
         uint32_t kx[3];
 #pragma unroll
         for (int y = -1; y <= 1; ++y) {
-            const int2 s = *reinterpret_cast<const int2*>(&sm.cell[base + x * g.ncy + y]);
+            const int2 s = *reinterpret_cast<const int2*>(&sm.cell[base + x + y * g.ncx]);
             const int dx4 = s.x - R4x, dy4 = s.y - R4y;
             kx[y + 1] = (uint32_t)(dx4 * dx4) + (uint32_t)(dy4 * dy4) + (uint32_t)(3 * (x + 1) + (y + 1));
         }
@@ -215,6 +217,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
     const bool colok = x0 + rx0 < a.wt;     // wt % 4 == 0: a group is all in or all out
     const int rows_here = min(TH, a.row_end - y0);
     const int L = a.L;
+    const bool want_lvl = a.level != nullptr;
     // tile row of this warp's j-th row, and whether its group exists
     auto row_of = [&](int j) { return warp + NW * j; };
     auto ok_of = [&](int j) { return colok && row_of(j) < rows_here; };
@@ -227,15 +230,15 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
     const int ncL1 = t1 ? gL1.ncx * gL1.ncy : 0;
     const CellGrid gL2 = cell_grid(x0, y0, L - 2, ncL + ncL1);
     const int ncL2 = t2 ? gL2.ncx * gL2.ncy : 0;
-    write_offtab(sm.offtab[0], gL.ncy);
-    write_offtab(sm.offtab[1], gL1.ncy);
-    write_offtab(sm.offtab[2], gL2.ncy);
+    write_offtab(sm.offtab[0], gL.ncx);
+    write_offtab(sm.offtab[1], gL1.ncx);
+    write_offtab(sm.offtab[2], gL2.ncx);
     for (int c = threadIdx.x; c < ncL + ncL1 + ncL2; c += NT) {
         const bool s0 = c < ncL, s1 = c < ncL + ncL1;
         CellGrid g;
         g.cx0 = s0 ? gL.cx0 : (s1 ? gL1.cx0 : gL2.cx0);
         g.cy0 = s0 ? gL.cy0 : (s1 ? gL1.cy0 : gL2.cy0);
-        g.ncy = s0 ? gL.ncy : (s1 ? gL1.ncy : gL2.ncy);
+        g.ncx = s0 ? gL.ncx : (s1 ? gL1.ncx : gL2.ncx);
         g.off = s0 ? 0 : (s1 ? ncL : ncL + ncL1);
         const int l = s0 ? L : (s1 ? L - 1 : L - 2);
         build_one(sm, a, gtf, x0, y0, l, level_salt(seed, l), g, c - g.off);
@@ -258,7 +261,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
             uint32_t cand[4];
             const uint32_t acc = group_eval(sm, a, gs, gL, sm.offtab[0], L, x0, y0, rx0, ry, gp4, cand);
             *reinterpret_cast<uint4*>(&sm.coord[ry * TW + rx0]) = make_uint4(cand[0], cand[1], cand[2], cand[3]);
-            *reinterpret_cast<uint32_t*>(&sm.lvl[ry * TW + rx0]) = 0x01010101u * (uint32_t)L;
+            if (want_lvl) *reinterpret_cast<uint32_t*>(&sm.lvl[ry * TW + rx0]) = 0x01010101u * (uint32_t)L;
             rej |= (~acc & 0xFu) << (4 * j);
         }
         if (t1) {
@@ -291,7 +294,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                     for (int i = 0; i < 4; ++i) {
                         if ((m >> i) & (acc >> i) & 1u) {
                             sm.coord[pbase + i] = cand[i];
-                            sm.lvl[pbase + i] = (uint8_t)l1;
+                            if (want_lvl) sm.lvl[pbase + i] = (uint8_t)l1;
                         }
                     }
                     still = m & ~acc;
@@ -351,7 +354,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                 const uint32_t gp = __ldg(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + rx));
                 if (accept(a, gs, gp, cand)) {
                     sm.coord[idx] = cand;
-                    sm.lvl[idx] = (uint8_t)l;
+                    if (want_lvl) sm.lvl[idx] = (uint8_t)l;
                 } else {
                     rej = true;
                 }
@@ -371,7 +374,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
             const int rx = idx & (TW - 1), ry = idx / TW;
             const uint32_t gp = __ldg(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + rx));
             sm.coord[idx] = __ldg(a.lut + (gp & 0xFFFFu));
-            sm.lvl[idx] = 0;
+            if (want_lvl) sm.lvl[idx] = 0;
         }
     }
     __syncwarp();
