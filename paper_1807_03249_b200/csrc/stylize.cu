@@ -290,12 +290,19 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                     const uint4 gp4 = *reinterpret_cast<const uint4*>(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + grx0));
                     uint32_t cand[4];
                     const uint32_t acc = group_eval(sm, a, gs, gL1, sm.offtab[1], l1, x0, y0, grx0, ry, gp4, cand);
+                    // merge the newly accepted pixels into the group's coords: one 16-byte
+                    // read-modify-write instead of four conflicting scalar stores
+                    const uint32_t take = m & acc;
+                    uint4 cv = *reinterpret_cast<const uint4*>(&sm.coord[pbase]);
+                    cv.x = (take & 1u) ? cand[0] : cv.x;
+                    cv.y = (take & 2u) ? cand[1] : cv.y;
+                    cv.z = (take & 4u) ? cand[2] : cv.z;
+                    cv.w = (take & 8u) ? cand[3] : cv.w;
+                    *reinterpret_cast<uint4*>(&sm.coord[pbase]) = cv;
+                    if (want_lvl) {
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        if ((m >> i) & (acc >> i) & 1u) {
-                            sm.coord[pbase + i] = cand[i];
-                            if (want_lvl) sm.lvl[pbase + i] = (uint8_t)l1;
-                        }
+                        for (int i = 0; i < 4; ++i)
+                            if ((take >> i) & 1u) sm.lvl[pbase + i] = (uint8_t)l1;
                     }
                     still = m & ~acc;
                 }
