@@ -25,6 +25,8 @@
 // NearestSeed ties: key = 16*d + i, i = 3*(x+1) + (y+1) in Alg. 2's loop order (x outer, y
 // inner), so the minimum key is the first strict minimum (reading R7).  d < 8 h^2 keeps the
 // key in 32 bits for h <= 2^12.
+#include <cstdlib>
+
 #include "sb_kernels.cuh"
 
 namespace sb {
@@ -413,6 +415,11 @@ cudaError_t launch_stylize_tiled(const StylizeArgs& a, int n_frames, cudaStream_
     const size_t smem = sizeof(Smem);
     cudaError_t e = cudaFuncSetAttribute(stylize_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    static const int carve = [] {
+        const char* ev = getenv("SB_STYLIZE_CARVEOUT");
+        return ev ? atoi(ev) : -1;
+    }();
+    if (carve >= 0) cudaFuncSetAttribute(stylize_tiled_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
     dim3 grid((unsigned)((a.wt + TW - 1) / TW), (unsigned)((a.row_end - a.row_begin + TH - 1) / TH),
               (unsigned)n_frames);
     stylize_tiled_kernel<<<grid, NT, smem, st>>>(a);
