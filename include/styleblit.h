@@ -56,6 +56,7 @@ typedef enum {
 /* sb_params.flags */
 #define SB_JITTER_ZERO 0x1u  /* RandomJitterTable == 0: seeds on the regular grid (tests)  */
 #define SB_NO_COLOR    0x2u  /* compute coords/levels only; ct may be NULL                 */
+#define SB_LABEL       0x4u  /* guide byte `label_channel` is a segmentation label (below)   */
 
 #define SB_MAX_LEVELS 12      /* level l uses spacing h = 2^l, l in [1, SB_MAX_LEVELS]       */
 #define SB_MAX_RADIUS 7       /* voting radius r in [0, SB_MAX_RADIUS]; (2r+1)^2*255 < 2^16   */
@@ -83,6 +84,15 @@ typedef struct {
      * (clipped) are written because the vote reads them.  Results equal the whole-frame
      * results.                                                                           */
     int32_t  row_begin, row_end;
+    /* Per-channel integer weights of the squared error: e^2 = sum_c w_c (G_T[p].c - G_S[s].c)^2
+     * over the first guide_channels bytes (SPEC compose_guides).  All zero = unit
+     * weights (the paper's plain norm).                                                   */
+    uint8_t  weights[4];
+    /* With SB_LABEL: guide byte label_channel (0..3) holds a segmentation label; a candidate
+     * whose label differs from the target pixel's is rejected at every level -- the
+     * "segmentation guide which prevents chunks to cross boundaries" of PAPER.md:514-517 --
+     * and that byte does not enter e.  (The level-0 look-up ignores labels.)              */
+    int32_t  label_channel;
 } sb_params;
 
 /* Bytes of device workspace sb_build_lut needs (65536 x 4). */

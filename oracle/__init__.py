@@ -44,6 +44,8 @@ class _Params(C.Structure):
         ("C", C.c_int32),
         ("seed", C.c_uint32),
         ("zero_jitter", C.c_int32),
+        ("w", C.c_int32 * 4),
+        ("label_channel", C.c_int32),
     ]
 
 
@@ -56,11 +58,14 @@ class Params:
     C: int = 3
     seed: int = 0x5EED
     zero_jitter: bool = False
+    weights: tuple = (1, 1, 1, 1)   # per-channel weights of e^2
+    label_channel: int | None = None  # segmentation label byte
 
     def c(self) -> _Params:
         # The GPU ABI takes t as float32; the oracle sees the same real number.
         return _Params(float(np.float32(self.t)), self.L, self.C, self.seed & 0xFFFFFFFF,
-                       1 if self.zero_jitter else 0)
+                       1 if self.zero_jitter else 0, (C.c_int32 * 4)(*[int(v) for v in self.weights]),
+                       -1 if self.label_channel is None else int(self.label_channel))
 
 
 _lib = None

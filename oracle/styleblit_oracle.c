@@ -161,10 +161,13 @@ void or_stylize_pixel(const or_params* prm, const uint8_t* gs, int32_t ws, int32
         int32_t sx = ux + (px - qx), sy = uy + (py - qy);                  /* u* + (p - q_l) */
         if (sx < 0 || sx >= ws || sy < 0 || sy >= hs) continue;           /* R9 */
         const uint8_t* gs_s = gs + 4 * ((int64_t)sy * ws + sx);
+        /* segmentation guide: a chunk never crosses a label boundary */
+        if (prm->label_channel >= 0 && gt_p[prm->label_channel] != gs_s[prm->label_channel]) continue;
         double e2 = 0.0;                                                   /* line 384, R1 */
         for (int32_t c = 0; c < prm->C; ++c) {
+            if (c == prm->label_channel) continue;
             double d = (double)gt_p[c] - (double)gs_s[c];
-            e2 += d * d;
+            e2 += (double)prm->w[c] * d * d;                               /* weighted channels */
         }
         double e = sqrt(e2);
         if (e < prm->t) {                                                  /* line 385, R3 */

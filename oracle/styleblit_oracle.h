@@ -29,6 +29,8 @@ typedef struct {
     int32_t  C;               /* guide channels used by the error e (R11, R18): 2..4           */
     uint32_t seed;            /* jitter-table seed (R5, R19)                                   */
     int32_t  zero_jitter;     /* 1: RandomJitterTable == 0 everywhere (test hook)              */
+    int32_t  w[4];            /* per-channel weights of e^2 (SPEC compose_guides)   */
+    int32_t  label_channel;   /* -1: none; else a segmentation label byte   */
 } or_params;
 
 /* R5 / SURVEY App. A: the stateless hash that realises RandomJitterTable. */

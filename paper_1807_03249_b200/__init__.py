@@ -18,11 +18,11 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import SB_JITTER_ZERO, SB_NO_COLOR, StyleBlitError, check, lib
+from ._lib import SB_JITTER_ZERO, SB_LABEL, SB_NO_COLOR, StyleBlitError, check, lib
 
 __all__ = [
     "Params", "build_lut", "stylize", "stylize_batch", "vote", "stylize_batch_host", "launch_count",
-    "version", "SB_JITTER_ZERO", "SB_NO_COLOR", "StyleBlitError",
+    "version", "SB_JITTER_ZERO", "SB_NO_COLOR", "SB_LABEL", "StyleBlitError",
 ]
 
 
@@ -38,11 +38,16 @@ class Params:
     flags: int = 0
     row_begin: int = 0
     row_end: int = 0
+    weights: tuple = (0, 0, 0, 0)  # per-channel integer weights; all zero = unit weights
+    label_channel: int | None = None  # segmentation label byte (sets SB_LABEL)
 
     def c(self) -> _lib.SbParams:
+        flags = int(self.flags) | (SB_LABEL if self.label_channel is not None else 0)
+        w = (C.c_uint8 * 4)(*[int(v) for v in self.weights])
         return _lib.SbParams(float(self.threshold), int(self.levels), int(self.blend_radius),
-                             int(self.guide_channels), int(self.seed) & 0xFFFFFFFF, int(self.flags),
-                             int(self.row_begin), int(self.row_end))
+                             int(self.guide_channels), int(self.seed) & 0xFFFFFFFF, flags,
+                             int(self.row_begin), int(self.row_end), w,
+                             -1 if self.label_channel is None else int(self.label_channel))
 
 
 def _dev(t: torch.Tensor, name: str, dtype: torch.dtype, ndim: tuple[int, ...]) -> int:

@@ -14,6 +14,7 @@ SO_PATH = os.path.join(HERE, "libstyleblit.so")
 SB_OK, SB_EINVAL, SB_EUNSUPPORTED, SB_ECUDA = 0, 1, 2, 3
 SB_JITTER_ZERO = 0x1
 SB_NO_COLOR = 0x2
+SB_LABEL = 0x4
 SB_MAX_LEVELS = 12
 SB_MAX_RADIUS = 7
 
@@ -35,6 +36,8 @@ class SbParams(C.Structure):
         ("flags", C.c_uint32),
         ("row_begin", C.c_int32),
         ("row_end", C.c_int32),
+        ("weights", C.c_uint8 * 4),
+        ("label_channel", C.c_int32),
     ]
 
 

@@ -69,7 +69,10 @@ sb_status validate(const sb_params* prm, int32_t n_frames, const uint8_t* cs, co
         return fail(SB_EINVAL, "blend_radius r=%d outside [0,%d]", prm->blend_radius, SB_MAX_RADIUS);
     if (prm->guide_channels < 2 || prm->guide_channels > 4)
         return fail(SB_EINVAL, "guide_channels C=%d not in {2,3,4}", prm->guide_channels);
-    if (prm->flags & ~(SB_JITTER_ZERO | SB_NO_COLOR)) return fail(SB_EINVAL, "flags 0x%x has unknown bits", prm->flags);
+    if (prm->flags & ~(SB_JITTER_ZERO | SB_NO_COLOR | SB_LABEL))
+        return fail(SB_EINVAL, "flags 0x%x has unknown bits", prm->flags);
+    if ((prm->flags & SB_LABEL) && (prm->label_channel < 0 || prm->label_channel > 3))
+        return fail(SB_EINVAL, "label_channel=%d outside [0,3]", prm->label_channel);
     int rb = prm->row_begin, re = prm->row_end;
     if (rb == 0 && re == 0) re = ht;
     if (rb < 0 || re > ht || rb >= re)
@@ -97,6 +100,18 @@ sb_status validate(const sb_params* prm, int32_t n_frames, const uint8_t* cs, co
     const double t2 = std::ceil((double)t * (double)t);  // exact: t is a float (reading R2)
     a.T2 = t2 >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)t2;
     a.cmask = prm->guide_channels == 4 ? 0xFFFFFFFFu : (prm->guide_channels == 3 ? 0x00FFFFFFu : 0x0000FFFFu);
+    const bool unit = (prm->weights[0] | prm->weights[1] | prm->weights[2] | prm->weights[3]) == 0;
+    bool ones = true;
+    for (int c = 0; c < 4; ++c) {
+        a.w[c] = unit ? 1u : prm->weights[c];
+        if (c < prm->guide_channels && a.w[c] != 1u) ones = false;
+    }
+    a.lmask = 0;
+    if (prm->flags & SB_LABEL) {
+        a.lmask = 0xFFu << (8 * prm->label_channel);
+        a.cmask &= ~a.lmask;  // the label byte does not enter e
+    }
+    a.ext = (!ones || a.lmask) ? 1 : 0;
     a.zero_jitter = (prm->flags & SB_JITTER_ZERO) ? 1 : 0;
     a.seed_base = prm->seed;
     a.coords = coords;

@@ -47,6 +47,20 @@ __device__ __forceinline__ uint32_t guide_d2(uint32_t a, uint32_t b, uint32_t cm
     return __dp4a(d, d, 0u);
 }
 
+// Extended test (weights, segmentation label): e^2 = sum_c w_c d_c^2 over the cmask bytes
+// (w_c d_c^2 <= 255*65025, the sum of four < 2^32), and equal labels under lmask.
+__device__ __forceinline__ bool guide_ok_ext(uint32_t a, uint32_t b, uint32_t cmask, const uint32_t* w,
+                                             uint32_t lmask, uint32_t T2) {
+    const uint32_t d = __vabsdiffu4(a, b) & cmask;
+    uint32_t D = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const uint32_t dc = (d >> (8 * c)) & 0xFFu;
+        D += w[c] * dc * dc;
+    }
+    return (D < T2) & (((a ^ b) & lmask) == 0u);
+}
+
 __device__ __forceinline__ uint32_t pack_xy(int x, int y) { return (uint32_t)x | ((uint32_t)y << 16); }
 
 // Streaming (evict-first) 128-bit global stores for outputs written once.

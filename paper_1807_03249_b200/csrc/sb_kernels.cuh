@@ -20,6 +20,9 @@ struct StylizeArgs {
     int L;
     uint32_t T2;        // accept iff D < T2 (= ceil(t*t), saturated)
     uint32_t cmask;     // guide channel byte mask for D
+    int ext;            // weighted channels and/or segmentation label in use
+    uint32_t w[4];      // per-channel weights (ext)
+    uint32_t lmask;     // byte mask of the segmentation label (ext; 0 = none)
     int zero_jitter;
     int row_begin, row_end;  // rows computed
     uint32_t seed_base;

@@ -107,17 +107,21 @@ __device__ __forceinline__ int warp_excl_scan(int v, int* total) {
 // Candidate test of Alg. 2 lines 384-385 on the packed candidate c = s.x | s.y<<16:
 // s inside the source (R9; a negative component borrows into a field >= 0x8000 > 32767)
 // and D = ||G_T[p] - G_S[s]||^2 < T2.  Branch-free: an outside candidate reads G_S[0].
+template <bool EXT>
 __device__ __forceinline__ bool accept(const StylizeArgs& a, const uint32_t* __restrict__ gs, uint32_t gp,
                                        uint32_t c) {
     const uint32_t x = c & 0xFFFFu, y = c >> 16;
     const bool inb = (x < (uint32_t)a.ws) & (y < (uint32_t)a.hs);
     const uint32_t gi = inb ? y * (uint32_t)a.ws + x : 0u;
-    return inb & (guide_d2(gp, __ldg(gs + gi), a.cmask) < a.T2);
+    const uint32_t g = __ldg(gs + gi);
+    if (EXT) return inb & guide_ok_ext(gp, g, a.cmask, a.w, a.lmask, a.T2);
+    return inb & (guide_d2(gp, g, a.cmask) < a.T2);
 }
 
 // Alg. 2 at level l (h >= 4) for the 4 pixels (px0..px0+3, py) that share one cell: the 9
 // seed loads and dy terms are shared, key_i = 16*((dx - i)^2 + dy^2) + idx = A - 8 i dx4 +
 // 16 i^2.  Writes the 4 packed candidates; returns the acceptance bits.
+template <bool EXT>
 __device__ __forceinline__ uint32_t group_eval(const Smem& sm, const StylizeArgs& a, const uint32_t* __restrict__ gs,
                                                const CellGrid& g, const int* offtab, int l, int x0, int y0, int rx0,
                                                int ry, uint4 gp4, uint32_t cand[4]) {
@@ -147,7 +151,7 @@ __device__ __forceinline__ uint32_t group_eval(const Smem& sm, const StylizeArgs
     for (int i = 0; i < 4; ++i) {
         const uint32_t c = p0 + (uint32_t)i + (uint32_t)sm.cell[base + offtab[keys[i] & 15u]].z;
         cand[i] = c;
-        acc |= (uint32_t)accept(a, gs, gpv[i], c) << i;
+        acc |= (uint32_t)accept<EXT>(a, gs, gpv[i], c) << i;
     }
     return acc;
 }
@@ -200,6 +204,7 @@ __device__ __forceinline__ uint32_t direct_candidate(const StylizeArgs& a, const
 
 }  // namespace
 
+template <bool EXT>
 __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_constant__ StylizeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -261,7 +266,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
             const int ry = row_of(j);
             const uint4 gp4 = ld_stream_u4(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + rx0), pol);
             uint32_t cand[4];
-            const uint32_t acc = group_eval(sm, a, gs, gL, sm.offtab[0], L, x0, y0, rx0, ry, gp4, cand);
+            const uint32_t acc = group_eval<EXT>(sm, a, gs, gL, sm.offtab[0], L, x0, y0, rx0, ry, gp4, cand);
             *reinterpret_cast<uint4*>(&sm.coord[ry * TW + rx0]) = make_uint4(cand[0], cand[1], cand[2], cand[3]);
             if (want_lvl) *reinterpret_cast<uint32_t*>(&sm.lvl[ry * TW + rx0]) = 0x01010101u * (uint32_t)L;
             rej |= (~acc & 0xFu) << (4 * j);
@@ -291,7 +296,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                     pbase = ry * TW + grx0;
                     const uint4 gp4 = *reinterpret_cast<const uint4*>(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + grx0));
                     uint32_t cand[4];
-                    const uint32_t acc = group_eval(sm, a, gs, gL1, sm.offtab[1], l1, x0, y0, grx0, ry, gp4, cand);
+                    const uint32_t acc = group_eval<EXT>(sm, a, gs, gL1, sm.offtab[1], l1, x0, y0, grx0, ry, gp4, cand);
                     // merge the newly accepted pixels into the group's coords: one 16-byte
                     // read-modify-write instead of four conflicting scalar stores
                     const uint32_t take = m & acc;
@@ -361,7 +366,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                 const uint32_t cand = table ? table_candidate(sm, g, offtab, l, x0, y0, rx, ry)
                                             : direct_candidate(a, gtf, x0 + rx, y0 + ry, l, c_l);
                 const uint32_t gp = __ldg(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + rx));
-                if (accept(a, gs, gp, cand)) {
+                if (accept<EXT>(a, gs, gp, cand)) {
                     sm.coord[idx] = cand;
                     if (want_lvl) sm.lvl[idx] = (uint8_t)l;
                 } else {
@@ -413,16 +418,17 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
 cudaError_t launch_stylize_tiled(const StylizeArgs& a, int n_frames, cudaStream_t st, int* launches) {
     static_assert(sizeof(Smem) <= 48 * 1024, "smem");
     const size_t smem = sizeof(Smem);
-    cudaError_t e = cudaFuncSetAttribute(stylize_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = a.ext ? stylize_tiled_kernel<true> : stylize_tiled_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     static const int carve = [] {
         const char* ev = getenv("SB_STYLIZE_CARVEOUT");
         return ev ? atoi(ev) : -1;
     }();
-    if (carve >= 0) cudaFuncSetAttribute(stylize_tiled_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+    if (carve >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
     dim3 grid((unsigned)((a.wt + TW - 1) / TW), (unsigned)((a.row_end - a.row_begin + TH - 1) / TH),
               (unsigned)n_frames);
-    stylize_tiled_kernel<<<grid, NT, smem, st>>>(a);
+    kern<<<grid, NT, smem, st>>>(a);
     *launches += 1;
     return cudaPeekAtLastError();
 }

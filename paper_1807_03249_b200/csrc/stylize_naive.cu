@@ -6,7 +6,8 @@
 
 namespace sb {
 
-__global__ void __launch_bounds__(256) stylize_naive_kernel(StylizeArgs a) {
+template <bool EXT>
+__global__ void __launch_bounds__(256) stylize_naive_kernel(const __grid_constant__ StylizeArgs a) {
     const int frame = blockIdx.y;
     const int64_t npx = (int64_t)(a.row_end - a.row_begin) * a.wt;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -42,8 +43,9 @@ __global__ void __launch_bounds__(256) stylize_naive_kernel(StylizeArgs a) {
         const int sx = (int)(u & 0xFFFFu) + (px - qx);
         const int sy = (int)(u >> 16) + (py - qy);
         if ((unsigned)sx >= (unsigned)a.ws || (unsigned)sy >= (unsigned)a.hs) continue;  // R9
-        const uint32_t d2 = guide_d2(gp, __ldg(gs + (int64_t)sy * a.ws + sx), a.cmask);
-        if (d2 < a.T2) { coord = pack_xy(sx, sy); level = l; break; }
+        const uint32_t g = __ldg(gs + (int64_t)sy * a.ws + sx);
+        const bool ok = EXT ? guide_ok_ext(gp, g, a.cmask, a.w, a.lmask, a.T2) : guide_d2(gp, g, a.cmask) < a.T2;
+        if (ok) { coord = pack_xy(sx, sy); level = l; break; }
     }
     if (level == 0) coord = __ldg(a.lut + (gp & 0xFFFFu));  // R12
     const int64_t o = fpx * frame + (int64_t)py * a.wt + px;
@@ -58,7 +60,8 @@ __global__ void __launch_bounds__(256) stylize_naive_kernel(StylizeArgs a) {
 cudaError_t launch_stylize_naive(const StylizeArgs& a, int n_frames, cudaStream_t st, int* launches) {
     const int64_t npx = (int64_t)(a.row_end - a.row_begin) * a.wt;
     dim3 grid((unsigned)((npx + 255) / 256), (unsigned)n_frames);
-    stylize_naive_kernel<<<grid, 256, 0, st>>>(a);
+    if (a.ext) stylize_naive_kernel<true><<<grid, 256, 0, st>>>(a);
+    else stylize_naive_kernel<false><<<grid, 256, 0, st>>>(a);
     *launches += 1;
     return cudaPeekAtLastError();
 }

@@ -189,17 +189,29 @@ def render_objects(W: int, H: int, seed: int = 2, device="cpu") -> torch.Tensor:
     return out
 
 
-def uv_identity(W: int, H: int, device="cpu") -> torch.Tensor:
-    """G5: (round(255x/(W-1)), round(255y/(H-1)), 0, 0); injective when W, H <= 256."""
+def _region_label(u: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
+    """A segmentation guide: 5 'semantic regions' of the UV square (a
+    central disc and four quadrants), labels 0, 64, 128, 192, 255 -- spaced far apart."""
+    lab = (64 * ((u >= 0.5).to(torch.int32) + 2 * (v >= 0.5).to(torch.int32))).to(torch.int32)
+    disc = (u - 0.5) ** 2 + (v - 0.45) ** 2 < 0.04
+    return torch.where(disc, torch.full_like(lab, 255), lab).to(torch.uint8)
+
+
+def uv_identity(W: int, H: int, device="cpu", labels: bool = False) -> torch.Tensor:
+    """G5: (round(255x/(W-1)), round(255y/(H-1)), 0, label); injective when W, H <= 256.
+    With labels=True channel 3 holds the region label of the UV position."""
     x, y = _grid(W, H, device)
     out = torch.zeros(H, W, 4, dtype=torch.uint8, device=device)
-    out[..., 0] = torch.floor(255.0 * x / max(W - 1, 1) + 0.5).to(torch.uint8)
-    out[..., 1] = torch.floor(255.0 * y / max(H - 1, 1) + 0.5).to(torch.uint8)
+    u, v = x / max(W - 1, 1), y / max(H - 1, 1)
+    out[..., 0] = torch.floor(255.0 * u + 0.5).to(torch.uint8)
+    out[..., 1] = torch.floor(255.0 * v + 0.5).to(torch.uint8)
+    if labels:
+        out[..., 3] = _region_label(u, v)
     return out
 
 
 def warp_uv(W: int, H: int, seed: int = 4, n_rbf: int = 8, amp: float = 40.0,
-            sigma: float = 170.0, device="cpu") -> torch.Tensor:
+            sigma: float = 170.0, device="cpu", labels: bool = False) -> torch.Tensor:
     """G6: G5 evaluated at clamp(p + sum_k A_k exp(-|p-c_k|^2 / 2 sigma^2)) (a smooth
     displacement field, the synthetic stand-in for FaceStyle's landmark warp)."""
     rng = np.random.RandomState(seed)
@@ -216,8 +228,11 @@ def warp_uv(W: int, H: int, seed: int = 4, n_rbf: int = 8, amp: float = 40.0,
     wx = torch.clamp(x + dx, 0, W - 1)
     wy = torch.clamp(y + dy, 0, H - 1)
     out = torch.zeros(H, W, 4, dtype=torch.uint8, device=device)
-    out[..., 0] = torch.floor(255.0 * wx / max(W - 1, 1) + 0.5).to(torch.uint8)
-    out[..., 1] = torch.floor(255.0 * wy / max(H - 1, 1) + 0.5).to(torch.uint8)
+    u, v = wx / max(W - 1, 1), wy / max(H - 1, 1)
+    out[..., 0] = torch.floor(255.0 * u + 0.5).to(torch.uint8)
+    out[..., 1] = torch.floor(255.0 * v + 0.5).to(torch.uint8)
+    if labels:
+        out[..., 3] = _region_label(u, v)
     return out
 
 

@@ -454,3 +454,53 @@ def test_vote_threads_identical():
     prm, cs, gs, gt, lut = _cfg1()
     _, coords, _ = oracle.stylize(prm, cs, gs, lut, gt)
     assert (oracle.vote(coords, cs, 2, 1) == oracle.vote(coords, cs, 2, 5)).all()
+
+
+# ------------------------------------------------------------------ NEXT #1: weighted guides, segmentation
+def test_weighted_3_4_5():
+    """Weighted error e^2 = sum w_c d_c^2 (SPEC compose_guides): (153,204) vs (0,0)
+    with w = (4,1): e^2 = 4*153^2 + 204^2 = 135252, e = 367.77 -> reject at t = 367, accept at 368."""
+    gt = np.array([[[153, 204, 0, 0]]], np.uint8)
+    gs = np.zeros((1, 1, 4), np.uint8)
+    lut = oracle.build_lut(gs)
+    for t, ok in ((367.0, False), (368.0, True)):
+        prm = oracle.Params(t=t, L=1, C=2, weights=(4, 1, 1, 1))
+        assert (oracle.stylize_pixel(prm, gs, lut, gt, 0, 0)[1] == 1) == ok
+
+
+def test_zero_weight_equals_fewer_channels():
+    """w_2 = 0 with C = 3 is C = 2 (a dropped channel), on a whole frame."""
+    prm, cs, gs, gt, lut = _cfg1(t=20.0)
+    a = oracle.stylize(oracle.Params(t=20.0, L=3, C=3, weights=(1, 1, 0, 1)), cs, gs, lut, gt)
+    b = oracle.stylize(oracle.Params(t=20.0, L=3, C=2), cs, gs, lut, gt)
+    c = oracle.stylize(oracle.Params(t=20.0, L=3, C=3), cs, gs, lut, gt)
+    assert all((x == y).all() for x, y in zip(a, b))
+    assert any((x != y).any() for x, y in zip(a, c))  # the channel mattered without the weight
+
+
+def test_segmentation_never_crosses_labels():
+    """with a segmentation label no accepted chunk crosses a region
+    boundary -- every pixel accepted at a level >= 1 copies from a source pixel with its own
+    label, even at a threshold that accepts everything else; the label byte is not part of e."""
+    W = H = 64
+    gs = synth.uv_identity(W, H, labels=True).numpy()
+    gt = synth.warp_uv(W, H, seed=4, amp=200.0, sigma=200.0).numpy()  # ~12 px displacements at 64^2
+    gt[..., 3] = synth.uv_identity(W, H, labels=True).numpy()[..., 3]  # regions of the target frame
+    cs = synth.painted_style(W, H).numpy()
+    lut = oracle.build_lut(gs)
+    prm_nolab = oracle.Params(t=1000.0, L=4, C=2)
+    prm_lab = oracle.Params(t=1000.0, L=4, C=2, label_channel=3)
+    _, c0, l0 = oracle.stylize(prm_nolab, cs, gs, lut, gt)
+    _, c1, l1 = oracle.stylize(prm_lab, cs, gs, lut, gt)
+    sx, sy = c1 & 0xFFFF, c1 >> 16
+    acc = l1 > 0
+    assert (gs[sy, sx, 3][acc] == gt[..., 3][acc]).all()
+    sx0, sy0 = c0 & 0xFFFF, c0 >> 16
+    assert (gs[sy0, sx0, 3][l0 > 0] != gt[..., 3][l0 > 0]).any()  # without labels chunks do cross
+    # the label byte does not enter e: with equal labels everywhere the result is unchanged
+    gt2, gs2 = gt.copy(), gs.copy()
+    gt2[..., 3] = 7
+    gs2[..., 3] = 7
+    a = oracle.stylize(oracle.Params(t=9.0, L=4, C=4, label_channel=3), cs, gs2, lut, gt2)
+    b = oracle.stylize(oracle.Params(t=9.0, L=4, C=3), cs, gs2, lut, gt2)
+    assert all((x == y).all() for x, y in zip(a, b))

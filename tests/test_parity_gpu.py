@@ -309,3 +309,47 @@ def test_outputs_fully_written(cid, r):
         res.append((ct, co, lv))
     for a_, b_ in zip(*res):
         assert torch.equal(a_, b_)
+
+
+@pytest.mark.parametrize("case", ["uv_labels", "uv_weights_labels", "normal_weights", "ragged_labels"])
+def test_weighted_and_segmentation_parity(case):
+    """per-channel weights and a segmentation label --
+    GPU == oracle on coords, levels and colours."""
+    if case.startswith("uv"):
+        W = 512
+        gs = synth.uv_identity(W, W, labels=True)
+        cs = synth.painted_style(W, W)
+        gt = synth.warp_uv(W, W, seed=4, labels=True)
+        gt[..., 3] = synth.uv_identity(W, W, labels=True)[..., 3]
+        kw = dict(threshold=2.5, levels=5, guide_channels=2, label_channel=3)
+        okw = dict(t=2.5, L=5, C=2, label_channel=3)
+        if case == "uv_weights_labels":
+            kw["weights"] = (3, 1, 0, 0)
+            okw["weights"] = (3, 1, 0, 0)
+    elif case == "normal_weights":
+        cfg = synth.CONFIGS[2]
+        cs, gs = synth.exemplar(cfg)
+        gt = synth.render_objects(640, 384, seed=2)
+        kw = dict(threshold=20.0, levels=5, guide_channels=3, weights=(2, 1, 3, 0))
+        okw = dict(t=20.0, L=5, C=3, weights=(2, 1, 3, 0))
+    else:
+        cs, gs, gt = _rand_case(131, 45, 48, 40, seed=3)
+        gt = gt.clone()
+        gs = gs.clone()
+        gt[..., 3] = (torch.arange(131)[None, :] // 40 * 60).to(torch.uint8).expand(45, 131)
+        gs[..., 3] = (torch.arange(48)[None, :] // 12 * 60).to(torch.uint8).expand(40, 48)
+        kw = dict(threshold=30.0, levels=3, guide_channels=3, label_channel=3)
+        okw = dict(t=30.0, L=3, C=3, label_channel=3)
+    csd, gsd, gtd = cs.to(DEV), gs.to(DEV), gt.to(DEV)
+    lut_d = sb.build_lut(gsd)
+    lut = oracle_lut(gs.numpy())
+    o = oracle.stylize(oracle.Params(seed=0x5EED, **okw), cs.numpy(), gs.numpy(), lut, gt.numpy(), nthreads=NTH)
+    for r in (0, 2):
+        ct, co, lv = sb.stylize(sb.Params(blend_radius=r, seed=0x5EED, **kw), csd, gsd, lut_d, gtd)
+        assert (u32(co) == o[1]).all() and (lv.cpu().numpy() == o[2]).all()
+        want = o[0] if r == 0 else oracle.vote(o[1], cs.numpy(), r, nthreads=NTH)
+        assert (ct.cpu().numpy() == want).all()
+    if "label" in case:
+        sx, sy = o[1] & 0xFFFF, o[1] >> 16
+        acc = o[2] > 0
+        assert (gs.numpy()[sy, sx, 3][acc] == gt.numpy()[..., 3][acc]).all()
