@@ -377,7 +377,7 @@ def cpu_baseline(args):
     t_lut, t_frames, *_ = oracle_sample(n, args.blend_radius, nth)
     tot = t_lut + t_frames
     return {"value": round(n * WT * HT / tot / 1e6, 3), "unit": "MP/s", "cores": nth, "kind": "oracle",
-            "sample": f"LUT build + {n} 4K frames (stylize + vote r={args.blend_radius}) of the cfg5 workload on "
+            "sample": f"LUT build + {n} 4K frames (stylize{" + vote r=" + str(args.blend_radius) if args.blend_radius else ", blit colours"}) of the cfg5 workload on "
                       f"{nth} host threads; {tot:.1f} s (LUT {t_lut:.1f} s)"}
 
 
@@ -417,7 +417,7 @@ def run_reference(args):
         "config": {"workload": f"cfg5: 4K UHD frames, 512x512 exemplar, L={cfg['L']}, t={cfg['t']}, C={cfg['C']}, "
                                f"blend r={r}; reference step = 1 frame on the CPU oracle (LUT built before timing)"},
         "cpu_baseline": {"value": v, "unit": "MP/s", "cores": nth, "kind": "oracle",
-                         "sample": f"1 4K frame per step (stylize + vote r={r}), {nth} host threads"},
+                         "sample": f"1 4K frame per step (stylize{" + vote r=" + str(r) if r else ", blit colours"}), {nth} host threads"},
         "e2e": {"value": v, "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     return out, rank, world
