@@ -14,7 +14,7 @@ for r in rows[1:]:
     us = float(r[vi].replace(",", "")) * scale.get(r[ui], 1e-3)
     c, t = agg.get(name, (0, 0.0))
     agg[name] = (c + 1, t + us)
-mine = {k: v for k, v in agg.items() if k.startswith("sb::") or "vote_kernel" in k}
+mine = {k: v for k, v in agg.items() if "sb::" in k}
 tot = sum(t for _, t in mine.values())
 print(f"{'kernel':45s} {'launches':>8s} {'total_us':>10s} {'mean_us':>9s} {'share':>6s}")
 for k, (c, t) in sorted(mine.items(), key=lambda kv: -kv[1][1]):
