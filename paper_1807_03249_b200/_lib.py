@@ -10,6 +10,8 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(HERE, "libstyleblit.so")
+# development hook for A/B timing of kernel variants: another build of the same library
+SO_PATH = os.environ.get("SB_LIBRARY", SO_PATH)
 
 SB_OK, SB_EINVAL, SB_EUNSUPPORTED, SB_ECUDA = 0, 1, 2, 3
 SB_JITTER_ZERO = 0x1

@@ -37,14 +37,15 @@ sb_status check_dims(const char* name, int32_t w, int32_t h) {
     return SB_OK;
 }
 
-// Which stylize kernel: the tiled kernel needs wt % 4 == 0 (uint4 pixel groups per row);
+// Which stylize kernel: the tiled kernel needs wt % 4 == 0 (uint4 pixel groups per row) and
+// L <= 9 (its tabled NearestSeed keys 1024 d + code fit 32 bits for h <= 2^9, stylize.cu);
 // SB_KERNEL=naive selects the one-thread-per-pixel kernel (for A/B measurement).
-bool use_naive(int32_t wt) {
+bool use_naive(int32_t wt, int32_t L) {
     static const int forced = [] {
         const char* e = getenv("SB_KERNEL");
         return (e && strcmp(e, "naive") == 0) ? 1 : 0;
     }();
-    return forced || (wt % 4) != 0;
+    return forced || (wt % 4) != 0 || L > 9;
 }
 
 struct Prepared {
@@ -142,7 +143,7 @@ sb_status launch_frames(Prepared& p, int n_frames, const uint32_t* frame_seeds, 
         a.has_seeds = frame_seeds ? 1 : 0;
         a.seed_base = seed_base_f0 + (uint32_t)f0;
         if (frame_seeds) memcpy(a.seeds, frame_seeds + f0, sizeof(uint32_t) * nf);
-        cudaError_t e = use_naive(a.wt) ? sb::launch_stylize_naive(a, nf, st, &g_launches)
+        cudaError_t e = use_naive(a.wt, a.L) ? sb::launch_stylize_naive(a, nf, st, &g_launches)
                                         : sb::launch_stylize_tiled(a, nf, st, &g_launches);
         if (e != cudaSuccess) return cuda_fail(e, "stylize launch");
         if (p.vote) {

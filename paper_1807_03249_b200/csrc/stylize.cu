@@ -41,7 +41,10 @@ constexpr int NW = NT / 32;       // warps per CTA
 constexpr int RPW = TH / NW;      // rows per warp (w, w + 8, ...)
 constexpr int WPX = TP / NW;      // pixels per warp
 // tables kept at once: levels {L, L-1, L-2} with h >= 4, i.e. at most levels 4, 3, 2
-constexpr int cells_of(int h) { return (TW / h + 3) * (TH / h + 3); }
+// Tables are column-major with a fixed column stride CS = 17 cells (272 bytes: odd in 16-byte
+// units, so lanes reading neighbouring columns hit different banks).  CS >= TH/4 + 3.
+constexpr int CS = 17;
+constexpr int cells_of(int h) { return (TW / h + 3) * CS; }
 constexpr int MAXCELLS = cells_of(4) + cells_of(8) + cells_of(16);
 
 struct Smem {
@@ -49,8 +52,7 @@ struct Smem {
     uint8_t lvl[TP];              // result levels
     uint16_t wq[NW][WPX];         // per-warp pixel queue (compacted in place)
     uint16_t glist[NW][RPW * NG]; // per-warp list of groups with a rejected pixel
-    int4 cell[MAXCELLS];          // seed/offset tables, row-major per level (cj*ncx + ci)
-    int offtab[3][16];            // winner offsets per table slot (L, L-1, L-2)
+    int4 cell[MAXCELLS];          // seed/offset tables, column-major per level (ci*CS + cj)
 };
 
 struct CellGrid {
@@ -69,9 +71,9 @@ __device__ __forceinline__ CellGrid cell_grid(int x0, int y0, int l, int off) {
 
 __device__ __forceinline__ void build_one(Smem& sm, const StylizeArgs& a, const uint32_t* __restrict__ gtf, int x0,
                                           int y0, int l, uint32_t c_l, const CellGrid& g, int c) {
-    // c < ncx*ncy <= 1000: (c + 0.5) / ncx is >= 0.007 away from an integer, float-exact floor
-    const int cj = (int)(((float)c + 0.5f) * __frcp_rn((float)g.ncx));
-    const int ci = c - cj * g.ncx;
+    // c < ncx*ncy <= 1000: (c + 0.5) / ncy is >= 0.007 away from an integer, float-exact floor
+    const int ci = (int)(((float)c + 0.5f) * __frcp_rn((float)g.ncy));
+    const int cj = c - ci * g.ncy;
     int sx, sy;
     cell_seed(g.cx0 + ci, g.cy0 + cj, l, c_l, a.zero_jitter != 0, sx, sy);
     const int qx = min(max(sx, 0), a.wt - 1);
@@ -79,15 +81,16 @@ __device__ __forceinline__ void build_one(Smem& sm, const StylizeArgs& a, const 
     const uint32_t u = __ldg(a.lut + (__ldg(gtf + (uint32_t)(qy * a.wt + qx)) & 0xFFFFu));
     // delta = u* - q packed as dy*65536 + dx: p_packed + delta is the packed candidate s
     const int dpack = ((int)(u >> 16) - qy) * 65536 + ((int)(u & 0xFFFFu) - qx);
-    sm.cell[g.off + c] = make_int4(4 * (sx - x0), 4 * (sy - y0), dpack, 0);
+    sm.cell[g.off + ci * CS + cj] = make_int4(32 * (sx - x0), 32 * (sy - y0), dpack, 0);
 }
 
-// Winner-offset table of a level: cell index offset of loop-order candidate i (0..8), i.e.
-// of cell (x, y) = (i/3 - 1, i%3 - 1) in the row-major table.  (Row-major so that lanes of a
-// warp, which sit in different cell columns, read different shared-memory banks.)
-__device__ __forceinline__ void write_offtab(int* tab, int ncx) {
-    if (threadIdx.x < 9) tab[threadIdx.x] = (int)(threadIdx.x / 3) - 1 + ((int)(threadIdx.x % 3) - 1) * ncx;
-}
+// NearestSeed key of a candidate: 1024 |s - p|^2 + code, code = 16 ((x+1) CS + (y+1)) = the
+// candidate's byte offset in the table relative to cell (-1,-1) of p.  Ordered by d, then by
+// Alg. 2's loop order (x outer, y inner): the minimum is the first strict minimum (reading R7),
+// and its low 10 bits address the winner's cell directly.  1024 d + code < 2^32 needs
+// d < 8 h^2 <= 2^22, i.e. h <= 2^9 for a tabled level (launcher: L <= 9 + ... see below).
+constexpr uint32_t code_of(int x, int y) { return 16u * (uint32_t)((x + 1) * CS + (y + 1)); }
+constexpr int CODE0 = 16 * (CS + 1);  // byte offset of cell (0,0) relative to cell (-1,-1)
 
 __device__ __forceinline__ uint32_t min3u(uint32_t a, uint32_t b, uint32_t c) { return min(min(a, b), c); }
 
@@ -118,64 +121,119 @@ __device__ __forceinline__ bool accept(const StylizeArgs& a, const uint32_t* __r
     return inb & (guide_d2(gp, g, a.cmask) < a.T2);
 }
 
+// NearestSeed (Alg. 2) for the 4 pixels (px0..px0+3, py) of a group, h >= 4:
+// they share their home cell, so the 9 seed loads and the dy terms are shared, and with
+// dx = 32 (s.x - px0), key_i = 1024 ((s.x - px0 - i)^2 + dy^2) + code = A - 64 i dx + 1024 i^2.
+// Returns the table address of cell (-1,-1) of the home cell; the winner of pixel i is the
+// cell at byte offset key[i] & 1023 from it.
+__device__ __forceinline__ const unsigned char* group_ns(const Smem& sm, const CellGrid& g, int l, int x0, int y0,
+                                                        int rx0, int ry, uint32_t key[4]) {
+    const int py = y0 + ry, px0 = x0 + rx0;
+    const int4* cb = &sm.cell[g.off + ((px0 >> l) - g.cx0 - 1) * CS + ((py >> l) - g.cy0 - 1)];
+    uint32_t k0 = 0xFFFFFFFFu, k1 = k0, k2 = k0, k3 = k0;
+    const int R32x = 32 * rx0, R32y = 32 * ry;
+#pragma unroll
+    for (int x = -1; x <= 1; ++x) {
+#pragma unroll
+        for (int y = -1; y <= 1; ++y) {
+            const int2 s = *reinterpret_cast<const int2*>(&cb[(x + 1) * CS + (y + 1)]);
+            const int dy = s.y - R32y;
+            const int dx = s.x - R32x;
+            const uint32_t A = (uint32_t)(dx * dx) + (uint32_t)(dy * dy) + code_of(x, y);
+            k0 = min(k0, A);
+            k1 = min(k1, A - 64u * (uint32_t)dx + 1024u);
+            k2 = min(k2, A - 128u * (uint32_t)dx + 4096u);
+            k3 = min(k3, A - 192u * (uint32_t)dx + 9216u);
+        }
+    }
+    key[0] = k0;
+    key[1] = k1;
+    key[2] = k2;
+    key[3] = k3;
+    return reinterpret_cast<const unsigned char*>(cb);
+}
+
+// delta = u* - q of the winning cell (the .z word of the table entry)
+__device__ __forceinline__ uint32_t winner_delta(const unsigned char* cb, uint32_t key) {
+    return (uint32_t)reinterpret_cast<const int4*>(cb + (key & 1023u))->z;
+}
+
 // Alg. 2 at level l (h >= 4) for the 4 pixels (px0..px0+3, py) that share one cell: the 9
 // seed loads and dy terms are shared, key_i = 16*((dx - i)^2 + dy^2) + idx = A - 8 i dx4 +
 // 16 i^2.  Writes the 4 packed candidates; returns the acceptance bits.
 template <bool EXT>
 __device__ __forceinline__ uint32_t group_eval(const Smem& sm, const StylizeArgs& a, const uint32_t* __restrict__ gs,
-                                               const CellGrid& g, const int* offtab, int l, int x0, int y0, int rx0,
-                                               int ry, uint4 gp4, uint32_t cand[4]) {
-    const int py = y0 + ry, px0 = x0 + rx0;
-    const int base = g.off + ((py >> l) - g.cy0) * g.ncx + ((px0 >> l) - g.cx0);
-    uint32_t k0 = 0xFFFFFFFFu, k1 = k0, k2 = k0, k3 = k0;
-    const int R4x = 4 * rx0, R4y = 4 * ry;
-#pragma unroll
-    for (int x = -1; x <= 1; ++x) {
-#pragma unroll
-        for (int y = -1; y <= 1; ++y) {
-            const int2 s = *reinterpret_cast<const int2*>(&sm.cell[base + x + y * g.ncx]);
-            const int dy4 = s.y - R4y;
-            const int dx4 = s.x - R4x;
-            const uint32_t A = (uint32_t)(dx4 * dx4) + (uint32_t)(dy4 * dy4) + (uint32_t)(3 * (x + 1) + (y + 1));
-            k0 = min(k0, A);
-            k1 = min(k1, A - 8u * (uint32_t)dx4 + 16u);
-            k2 = min(k2, A - 16u * (uint32_t)dx4 + 64u);
-            k3 = min(k3, A - 24u * (uint32_t)dx4 + 144u);
-        }
-    }
-    const uint32_t keys[4] = {k0, k1, k2, k3};
+                                               const CellGrid& g, int l, int x0, int y0, int rx0, int ry, uint4 gp4,
+                                               uint32_t cand[4]) {
+    uint32_t keys[4];
+    const unsigned char* cb = group_ns(sm, g, l, x0, y0, rx0, ry, keys);
     const uint32_t gpv[4] = {gp4.x, gp4.y, gp4.z, gp4.w};
-    const uint32_t p0 = ((uint32_t)py << 16) | (uint32_t)px0;
+    const uint32_t p0 = ((uint32_t)(y0 + ry) << 16) | (uint32_t)(x0 + rx0);
     uint32_t acc = 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const uint32_t c = p0 + (uint32_t)i + (uint32_t)sm.cell[base + offtab[keys[i] & 15u]].z;
+        const uint32_t c = p0 + (uint32_t)i + winner_delta(cb, keys[i]);
         cand[i] = c;
         acc |= (uint32_t)accept<EXT>(a, gs, gpv[i], c) << i;
     }
     return acc;
 }
 
+// group_eval split in two for software pipelining: group_issue does NearestSeed, forms the 4
+// candidates and issues their G_S gathers; group_test (called later, after other work has
+// covered the gather latency) applies the threshold.
+__device__ __forceinline__ uint32_t group_issue(const Smem& sm, const StylizeArgs& a, const uint32_t* __restrict__ gs,
+                                                const CellGrid& g, int l, int x0, int y0, int rx0, int ry,
+                                                uint32_t cand[4], uint32_t gv[4]) {
+    uint32_t keys[4];
+    const unsigned char* cb = group_ns(sm, g, l, x0, y0, rx0, ry, keys);
+    const uint32_t p0 = ((uint32_t)(y0 + ry) << 16) | (uint32_t)(x0 + rx0);
+    uint32_t inb = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t c = p0 + (uint32_t)i + winner_delta(cb, keys[i]);
+        cand[i] = c;
+        const uint32_t x = c & 0xFFFFu, y = c >> 16;
+        const bool in = (x < (uint32_t)a.ws) & (y < (uint32_t)a.hs);
+        gv[i] = __ldg(gs + (in ? y * (uint32_t)a.ws + x : 0u));
+        inb |= (uint32_t)in << i;
+    }
+    return inb;
+}
+
+template <bool EXT>
+__device__ __forceinline__ uint32_t group_test(const StylizeArgs& a, uint4 gp4, const uint32_t gv[4], uint32_t inb) {
+    const uint32_t gpv[4] = {gp4.x, gp4.y, gp4.z, gp4.w};
+    uint32_t acc = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const bool ok = EXT ? guide_ok_ext(gpv[i], gv[i], a.cmask, a.w, a.lmask, a.T2)
+                            : guide_d2(gpv[i], gv[i], a.cmask) < a.T2;
+        acc |= (uint32_t)ok << i;
+    }
+    return acc & inb;
+}
+
 // Alg. 2 at level l for one pixel from the level's shared-memory table.
-__device__ __forceinline__ uint32_t table_candidate(const Smem& sm, const CellGrid& g, const int* offtab, int l,
-                                                    int x0, int y0, int rx, int ry) {
+__device__ __forceinline__ uint32_t table_candidate(const Smem& sm, const CellGrid& g, int l, int x0, int y0, int rx,
+                                                    int ry) {
     const int px = x0 + rx, py = y0 + ry;
-    const int base = g.off + ((py >> l) - g.cy0) * g.ncx + ((px >> l) - g.cx0);
-    const int R4x = 4 * rx, R4y = 4 * ry;
+    const int4* cb = &sm.cell[g.off + ((px >> l) - g.cx0 - 1) * CS + ((py >> l) - g.cy0 - 1)];
+    const int R32x = 32 * rx, R32y = 32 * ry;
     uint32_t kk[3];
 #pragma unroll
     for (int x = -1; x <= 1; ++x) {
         uint32_t kx[3];
 #pragma unroll
         for (int y = -1; y <= 1; ++y) {
-            const int2 s = *reinterpret_cast<const int2*>(&sm.cell[base + x + y * g.ncx]);
-            const int dx4 = s.x - R4x, dy4 = s.y - R4y;
-            kx[y + 1] = (uint32_t)(dx4 * dx4) + (uint32_t)(dy4 * dy4) + (uint32_t)(3 * (x + 1) + (y + 1));
+            const int2 s = *reinterpret_cast<const int2*>(&cb[(x + 1) * CS + (y + 1)]);
+            const int dx = s.x - R32x, dy = s.y - R32y;
+            kx[y + 1] = (uint32_t)(dx * dx) + (uint32_t)(dy * dy) + code_of(x, y);
         }
         kk[x + 1] = min3u(kx[0], kx[1], kx[2]);
     }
     const uint32_t key = min3u(kk[0], kk[1], kk[2]);
-    return (((uint32_t)py << 16) | (uint32_t)px) + (uint32_t)sm.cell[base + offtab[key & 15u]].z;
+    return (((uint32_t)py << 16) | (uint32_t)px) + winner_delta(reinterpret_cast<const unsigned char*>(cb), key);
 }
 
 // Alg. 2 at level l for one pixel, NearestSeed straight from the hash.
@@ -232,23 +290,17 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
     // ---- tables of the levels among L, L-1, L-2 with h >= 4: the only CTA barrier ----
     const bool t0 = L >= 2, t1 = L - 1 >= 2, t2 = L - 2 >= 2;
     const CellGrid gL = cell_grid(x0, y0, L, 0);
+    // valid cells per level (built) and slots per level (column stride CS)
     const int ncL = t0 ? gL.ncx * gL.ncy : 0;
-    const CellGrid gL1 = cell_grid(x0, y0, L - 1, ncL);
+    const CellGrid gL1 = cell_grid(x0, y0, L - 1, gL.ncx * CS);
     const int ncL1 = t1 ? gL1.ncx * gL1.ncy : 0;
-    const CellGrid gL2 = cell_grid(x0, y0, L - 2, ncL + ncL1);
+    const CellGrid gL2 = cell_grid(x0, y0, L - 2, gL.ncx * CS + gL1.ncx * CS);
     const int ncL2 = t2 ? gL2.ncx * gL2.ncy : 0;
-    write_offtab(sm.offtab[0], gL.ncx);
-    write_offtab(sm.offtab[1], gL1.ncx);
-    write_offtab(sm.offtab[2], gL2.ncx);
     for (int c = threadIdx.x; c < ncL + ncL1 + ncL2; c += NT) {
         const bool s0 = c < ncL, s1 = c < ncL + ncL1;
-        CellGrid g;
-        g.cx0 = s0 ? gL.cx0 : (s1 ? gL1.cx0 : gL2.cx0);
-        g.cy0 = s0 ? gL.cy0 : (s1 ? gL1.cy0 : gL2.cy0);
-        g.ncx = s0 ? gL.ncx : (s1 ? gL1.ncx : gL2.ncx);
-        g.off = s0 ? 0 : (s1 ? ncL : ncL + ncL1);
+        const CellGrid& g = s0 ? gL : (s1 ? gL1 : gL2);
         const int l = s0 ? L : (s1 ? L - 1 : L - 2);
-        build_one(sm, a, gtf, x0, y0, l, level_salt(seed, l), g, c - g.off);
+        build_one(sm, a, gtf, x0, y0, l, level_salt(seed, l), g, c - (s0 ? 0 : (s1 ? ncL : ncL + ncL1)));
     }
     __syncthreads();
     // From here on a warp only touches its own rows: no further CTA barrier.
@@ -259,17 +311,40 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
     const uint64_t pol = policy_evict_first();
     if (L >= 2) {
         // ---- level L: every pixel, in 4-pixel groups; G_T streamed once from HBM ----
+        // Software-pipelined over the warp's rows: row j's NearestSeed and gathers are issued
+        // before row j-1's threshold test, so the G_T load and the G_S gathers of a row are
+        // in flight while the next row's NearestSeed runs.
         uint32_t rej = 0;  // 4 bits per row j
-#pragma unroll 2
-        for (int j = 0; j < RPW; ++j) {
-            if (!ok_of(j)) continue;
-            const int ry = row_of(j);
-            const uint4 gp4 = ld_stream_u4(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + rx0), pol);
-            uint32_t cand[4];
-            const uint32_t acc = group_eval<EXT>(sm, a, gs, gL, sm.offtab[0], L, x0, y0, rx0, ry, gp4, cand);
-            *reinterpret_cast<uint4*>(&sm.coord[ry * TW + rx0]) = make_uint4(cand[0], cand[1], cand[2], cand[3]);
-            if (want_lvl) *reinterpret_cast<uint32_t*>(&sm.lvl[ry * TW + rx0]) = 0x01010101u * (uint32_t)L;
-            rej |= (~acc & 0xFu) << (4 * j);
+        uint32_t pcand[4] = {0u, 0u, 0u, 0u}, pgv[4] = {0u, 0u, 0u, 0u}, pinb = 0;
+        uint4 pgp = make_uint4(0u, 0u, 0u, 0u);
+        bool pok = false;
+#pragma unroll
+        for (int j = 0; j <= RPW; ++j) {
+            uint32_t cand[4], gv[4], inb = 0;
+            uint4 gp4;
+            const bool ok = j < RPW && ok_of(j);
+            if (ok) {
+                const int ry = row_of(j);
+                gp4 = *reinterpret_cast<const uint4*>(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + rx0));
+                inb = group_issue(sm, a, gs, gL, L, x0, y0, rx0, ry, cand, gv);
+            }
+            if (pok) {
+                const int ry = row_of(j - 1);
+                const uint32_t acc = group_test<EXT>(a, pgp, pgv, pinb);
+                *reinterpret_cast<uint4*>(&sm.coord[ry * TW + rx0]) = make_uint4(pcand[0], pcand[1], pcand[2], pcand[3]);
+                if (want_lvl) *reinterpret_cast<uint32_t*>(&sm.lvl[ry * TW + rx0]) = 0x01010101u * (uint32_t)L;
+                rej |= (~acc & 0xFu) << (4 * (j - 1));
+            }
+            if (j < RPW) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    pcand[i] = cand[i];
+                    pgv[i] = gv[i];
+                }
+                pinb = inb;
+                pgp = gp4;
+                pok = ok;
+            }
         }
         if (t1) {
             // ---- level L-1 on the warp's groups that still have a rejected pixel ----
@@ -296,7 +371,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                     pbase = ry * TW + grx0;
                     const uint4 gp4 = *reinterpret_cast<const uint4*>(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + grx0));
                     uint32_t cand[4];
-                    const uint32_t acc = group_eval<EXT>(sm, a, gs, gL1, sm.offtab[1], l1, x0, y0, grx0, ry, gp4, cand);
+                    const uint32_t acc = group_eval<EXT>(sm, a, gs, gL1, l1, x0, y0, grx0, ry, gp4, cand);
                     // merge the newly accepted pixels into the group's coords: one 16-byte
                     // read-modify-write instead of four conflicting scalar stores
                     const uint32_t take = m & acc;
@@ -353,7 +428,6 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
     for (; l >= 1 && n > 0; --l) {
         const bool table = (l == L - 2 && t2) || (l == L - 1 && t1) || (l == L && t0);
         const CellGrid& g = (l == L) ? gL : ((l == L - 1) ? gL1 : gL2);
-        const int* offtab = sm.offtab[(l == L) ? 0 : ((l == L - 1) ? 1 : 2)];
         const uint32_t c_l = level_salt(seed, l);
         int nn = 0;
         for (int k0 = 0; k0 < n; k0 += 32) {
@@ -363,7 +437,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
             if (k < n) {
                 idx = q[k];
                 const int rx = idx & (TW - 1), ry = idx / TW;
-                const uint32_t cand = table ? table_candidate(sm, g, offtab, l, x0, y0, rx, ry)
+                const uint32_t cand = table ? table_candidate(sm, g, l, x0, y0, rx, ry)
                                             : direct_candidate(a, gtf, x0 + rx, y0 + ry, l, c_l);
                 const uint32_t gp = __ldg(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + rx));
                 if (accept<EXT>(a, gs, gp, cand)) {
@@ -396,22 +470,32 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
     // ---- outputs: coords, levels, blit colours ----
     const uint32_t* __restrict__ cs = reinterpret_cast<const uint32_t*>(a.cs);
     const uint32_t ws = (uint32_t)a.ws;
-#pragma unroll 2
-    for (int j = 0; j < RPW; ++j) {
-        if (!ok_of(j)) continue;
-        const int ry = row_of(j);
-        const int64_t o = fpx * frame + (int64_t)((y0 + ry) * wt + (uint32_t)(x0 + rx0));
-        const uint4 cv = *reinterpret_cast<const uint4*>(&sm.coord[ry * TW + rx0]);
-        if (a.coords) st_cs_u4(a.coords + o, cv);
-        if (a.level) st_cs_u32(a.level + o, *reinterpret_cast<const uint32_t*>(&sm.lvl[ry * TW + rx0]));
-        if (a.ct) {
-            uint4 col;
-            col.x = __ldg(cs + ((cv.x >> 16) * ws + (cv.x & 0xFFFFu)));
-            col.y = __ldg(cs + ((cv.y >> 16) * ws + (cv.y & 0xFFFFu)));
-            col.z = __ldg(cs + ((cv.z >> 16) * ws + (cv.z & 0xFFFFu)));
-            col.w = __ldg(cs + ((cv.w >> 16) * ws + (cv.w & 0xFFFFu)));
-            st_cs_u4(a.ct + 4 * o, col);
+    // pipelined: row j's colour gathers are issued before row j-1's colours are stored
+    uint4 pcol = make_uint4(0u, 0u, 0u, 0u);
+    int64_t po = 0;
+    bool pok = false;
+#pragma unroll
+    for (int j = 0; j <= RPW; ++j) {
+        const bool ok = j < RPW && ok_of(j);
+        uint4 col;
+        int64_t o = 0;
+        if (ok) {
+            const int ry = row_of(j);
+            o = fpx * frame + (int64_t)((y0 + ry) * wt + (uint32_t)(x0 + rx0));
+            const uint4 cv = *reinterpret_cast<const uint4*>(&sm.coord[ry * TW + rx0]);
+            if (a.coords) st_cs_u4(a.coords + o, cv);
+            if (a.level) st_cs_u32(a.level + o, *reinterpret_cast<const uint32_t*>(&sm.lvl[ry * TW + rx0]));
+            if (a.ct) {
+                col.x = __ldg(cs + ((cv.x >> 16) * ws + (cv.x & 0xFFFFu)));
+                col.y = __ldg(cs + ((cv.y >> 16) * ws + (cv.y & 0xFFFFu)));
+                col.z = __ldg(cs + ((cv.z >> 16) * ws + (cv.z & 0xFFFFu)));
+                col.w = __ldg(cs + ((cv.w >> 16) * ws + (cv.w & 0xFFFFu)));
+            }
         }
+        if (pok && a.ct) st_cs_u4(a.ct + 4 * po, pcol);
+        pcol = col;
+        po = o;
+        pok = ok;
     }
 }
 
