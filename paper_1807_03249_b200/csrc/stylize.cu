@@ -41,15 +41,16 @@ constexpr int NW = NT / 32;       // warps per CTA
 constexpr int RPW = TH / NW;      // rows per warp (w, w + 8, ...)
 constexpr int WPX = TP / NW;      // pixels per warp
 // tables kept at once: levels {L, L-1, L-2} with h >= 4, i.e. at most levels 4, 3, 2
-// Tables are column-major with a fixed column stride CS = 17 cells (272 bytes: odd in 16-byte
-// units, so lanes reading neighbouring columns hit different banks).  CS >= TH/4 + 3.
-constexpr int CS = 17;
+// Tables are column-major with a fixed column stride CS = 13 cells (208 bytes = 52 words: 8
+// neighbouring columns start in 8 distinct even banks, so the 8-byte loads of lanes in
+// different columns do not conflict).  CS >= TH/4 + 4, the most cells a column of a level
+// with h = 4 spans.
+constexpr int CS = 13;
 constexpr int cells_of(int h) { return (TW / h + 3) * CS; }
 constexpr int MAXCELLS = cells_of(4) + cells_of(8) + cells_of(16);
 
 struct Smem {
     uint32_t coord[TP];           // result coords
-    uint8_t lvl[TP];              // result levels
     uint16_t wq[NW][WPX];         // per-warp pixel queue (compacted in place)
     uint16_t glist[NW][RPW * NG]; // per-warp list of groups with a rejected pixel
     int4 cell[MAXCELLS];          // seed/offset tables, column-major per level (ci*CS + cj)
@@ -266,6 +267,7 @@ template <bool EXT>
 __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_constant__ StylizeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+    uint8_t* lvl = smem_raw + sizeof(Smem);  // result levels (only when a.level != nullptr)
 
     const int x0 = blockIdx.x * TW;
     const int y0 = a.row_begin + blockIdx.y * TH;
@@ -332,7 +334,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                 const int ry = row_of(j - 1);
                 const uint32_t acc = group_test<EXT>(a, pgp, pgv, pinb);
                 *reinterpret_cast<uint4*>(&sm.coord[ry * TW + rx0]) = make_uint4(pcand[0], pcand[1], pcand[2], pcand[3]);
-                if (want_lvl) *reinterpret_cast<uint32_t*>(&sm.lvl[ry * TW + rx0]) = 0x01010101u * (uint32_t)L;
+                if (want_lvl) *reinterpret_cast<uint32_t*>(&lvl[ry * TW + rx0]) = 0x01010101u * (uint32_t)L;
                 rej |= (~acc & 0xFu) << (4 * (j - 1));
             }
             if (j < RPW) {
@@ -384,7 +386,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                     if (want_lvl) {
 #pragma unroll
                         for (int i = 0; i < 4; ++i)
-                            if ((take >> i) & 1u) sm.lvl[pbase + i] = (uint8_t)l1;
+                            if ((take >> i) & 1u) lvl[pbase + i] = (uint8_t)l1;
                     }
                     still = m & ~acc;
                 }
@@ -442,7 +444,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                 const uint32_t gp = __ldg(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + rx));
                 if (accept<EXT>(a, gs, gp, cand)) {
                     sm.coord[idx] = cand;
-                    if (want_lvl) sm.lvl[idx] = (uint8_t)l;
+                    if (want_lvl) lvl[idx] = (uint8_t)l;
                 } else {
                     rej = true;
                 }
@@ -462,7 +464,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
             const int rx = idx & (TW - 1), ry = idx / TW;
             const uint32_t gp = __ldg(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + rx));
             sm.coord[idx] = __ldg(a.lut + (gp & 0xFFFFu));
-            if (want_lvl) sm.lvl[idx] = 0;
+            if (want_lvl) lvl[idx] = 0;
         }
     }
     __syncwarp();
@@ -470,38 +472,29 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
     // ---- outputs: coords, levels, blit colours ----
     const uint32_t* __restrict__ cs = reinterpret_cast<const uint32_t*>(a.cs);
     const uint32_t ws = (uint32_t)a.ws;
-    // pipelined: row j's colour gathers are issued before row j-1's colours are stored
-    uint4 pcol = make_uint4(0u, 0u, 0u, 0u);
-    int64_t po = 0;
-    bool pok = false;
-#pragma unroll
-    for (int j = 0; j <= RPW; ++j) {
-        const bool ok = j < RPW && ok_of(j);
-        uint4 col;
-        int64_t o = 0;
-        if (ok) {
-            const int ry = row_of(j);
-            o = fpx * frame + (int64_t)((y0 + ry) * wt + (uint32_t)(x0 + rx0));
-            const uint4 cv = *reinterpret_cast<const uint4*>(&sm.coord[ry * TW + rx0]);
-            if (a.coords) st_cs_u4(a.coords + o, cv);
-            if (a.level) st_cs_u32(a.level + o, *reinterpret_cast<const uint32_t*>(&sm.lvl[ry * TW + rx0]));
-            if (a.ct) {
-                col.x = __ldg(cs + ((cv.x >> 16) * ws + (cv.x & 0xFFFFu)));
-                col.y = __ldg(cs + ((cv.y >> 16) * ws + (cv.y & 0xFFFFu)));
-                col.z = __ldg(cs + ((cv.z >> 16) * ws + (cv.z & 0xFFFFu)));
-                col.w = __ldg(cs + ((cv.w >> 16) * ws + (cv.w & 0xFFFFu)));
-            }
+#pragma unroll 2
+    for (int j = 0; j < RPW; ++j) {
+        if (!ok_of(j)) continue;
+        const int ry = row_of(j);
+        const int64_t o = fpx * frame + (int64_t)((y0 + ry) * wt + (uint32_t)(x0 + rx0));
+        const uint4 cv = *reinterpret_cast<const uint4*>(&sm.coord[ry * TW + rx0]);
+        if (a.coords) st_cs_u4(a.coords + o, cv);
+        if (a.level) st_cs_u32(a.level + o, *reinterpret_cast<const uint32_t*>(&lvl[ry * TW + rx0]));
+        if (a.ct) {
+            uint4 col;
+            col.x = __ldg(cs + ((cv.x >> 16) * ws + (cv.x & 0xFFFFu)));
+            col.y = __ldg(cs + ((cv.y >> 16) * ws + (cv.y & 0xFFFFu)));
+            col.z = __ldg(cs + ((cv.z >> 16) * ws + (cv.z & 0xFFFFu)));
+            col.w = __ldg(cs + ((cv.w >> 16) * ws + (cv.w & 0xFFFFu)));
+            st_cs_u4(a.ct + 4 * o, col);
         }
-        if (pok && a.ct) st_cs_u4(a.ct + 4 * po, pcol);
-        pcol = col;
-        po = o;
-        pok = ok;
     }
 }
 
 cudaError_t launch_stylize_tiled(const StylizeArgs& a, int n_frames, cudaStream_t st, int* launches) {
-    static_assert(sizeof(Smem) <= 48 * 1024, "smem");
-    const size_t smem = sizeof(Smem);
+    static_assert(sizeof(Smem) + TP <= 48 * 1024, "smem");
+    // the level map only when requested: without it 4 CTAs leave ~92 KB of L1 per SM
+    const size_t smem = sizeof(Smem) + (a.level ? TP : 0);
     auto kern = a.ext ? stylize_tiled_kernel<true> : stylize_tiled_kernel<false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
