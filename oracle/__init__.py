@@ -46,6 +46,7 @@ class _Params(C.Structure):
         ("zero_jitter", C.c_int32),
         ("w", C.c_int32 * 4),
         ("label_channel", C.c_int32),
+        ("lut_rgb", C.c_int32),
     ]
 
 
@@ -60,12 +61,14 @@ class Params:
     zero_jitter: bool = False
     weights: tuple = (1, 1, 1, 1)   # per-channel weights of e^2
     label_channel: int | None = None  # segmentation label byte
+    lut_rgb: bool = False             # u* by exact search over channels 0..2 (R26)
 
     def c(self) -> _Params:
         # The GPU ABI takes t as float32; the oracle sees the same real number.
         return _Params(float(np.float32(self.t)), self.L, self.C, self.seed & 0xFFFFFFFF,
                        1 if self.zero_jitter else 0, (C.c_int32 * 4)(*[int(v) for v in self.weights]),
-                       -1 if self.label_channel is None else int(self.label_channel))
+                       -1 if self.label_channel is None else int(self.label_channel),
+                       1 if self.lut_rgb else 0)
 
 
 _lib = None
@@ -91,6 +94,9 @@ def lib():
                                        C.POINTER(C.c_uint32), C.POINTER(C.c_uint8)]
         l.or_stylize.argtypes = [C.POINTER(_Params), u8p, u8p, i32, i32, u32p, u8p, i32, i32, u8p, u32p, u8p, i32]
         l.or_vote.argtypes = [u32p, i32, i32, u8p, i32, i32, i32, u8p, i32]
+        l.or_lut3_entry.restype = C.c_uint32
+        l.or_lut3_entry.argtypes = [u8p, i32, i32, i32, i32, i32]
+        l.or_lut3_entries.argtypes = [u8p, i32, i32, u32p, C.c_int64, u32p, i32]
         l.or_version.restype = C.c_char_p
         _lib = l
     return _lib
@@ -101,7 +107,9 @@ def _u8(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_uint8))
 
 
-def _u32(a: np.ndarray):
+def _u32(a: np.ndarray | None):
+    if a is None:
+        return C.POINTER(C.c_uint32)()
     assert a.dtype == np.uint32 and a.flags.c_contiguous
     return a.ctypes.data_as(C.POINTER(C.c_uint32))
 
@@ -147,6 +155,20 @@ def nearest_seed(px: int, py: int, l: int, seed: int, zero_jitter: bool = False)
 def lut_entry(gs: np.ndarray, g0: int, g1: int) -> int:
     ws, hs = _img(gs)
     return lib().or_lut_entry(_u8(gs), ws, hs, g0, g1)
+
+
+def lut3_entry(gs: np.ndarray, g0: int, g1: int, g2: int) -> int:
+    ws, hs = _img(gs)
+    return lib().or_lut3_entry(_u8(gs), ws, hs, g0, g1, g2)
+
+
+def lut3_entries(gs: np.ndarray, keys: np.ndarray, nthreads: int = 1) -> np.ndarray:
+    """Exact 3-channel search for keys g0 | g1<<8 | g2<<16 (R26)."""
+    ws, hs = _img(gs)
+    keys = np.ascontiguousarray(keys, dtype=np.uint32)
+    out = np.zeros(keys.shape, np.uint32)
+    lib().or_lut3_entries(_u8(gs), ws, hs, _u32(keys), keys.size, _u32(out), nthreads)
+    return out
 
 
 def build_lut(gs: np.ndarray, nthreads: int = 1) -> np.ndarray:

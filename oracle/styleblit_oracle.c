@@ -113,6 +113,52 @@ uint32_t or_lut_entry(const uint8_t* gs, int32_t ws, int32_t hs, int32_t g0, int
     return best_u;
 }
 
+/* Exact guide search over three channels (the look-up "or a tree search";
+ * SURVEY 8(f) #3): u* = argmin_u ||(g0,g1,g2) - G_S[u].(c0,c1,c2)||, row-major scan, first
+ * strict minimum (the tie rule of R10).  Reading R26.                                     */
+uint32_t or_lut3_entry(const uint8_t* gs, int32_t ws, int32_t hs, int32_t g0, int32_t g1, int32_t g2) {
+    int64_t best = -1;
+    uint32_t best_u = 0;
+    for (int32_t y = 0; y < hs; ++y) {
+        for (int32_t x = 0; x < ws; ++x) {
+            const uint8_t* g = gs + 4 * ((int64_t)y * ws + x);
+            int64_t d0 = (int64_t)g0 - g[0], d1 = (int64_t)g1 - g[1], d2 = (int64_t)g2 - g[2];
+            int64_t d = d0 * d0 + d1 * d1 + d2 * d2;
+            if (best < 0 || d < best) { best = d; best_u = (uint32_t)x | ((uint32_t)y << 16); }
+        }
+    }
+    return best_u;
+}
+
+typedef struct {
+    const uint8_t* gs; int32_t ws, hs; const uint32_t* keys; uint32_t* out; int64_t b, e;
+} lut3_job;
+
+static void* lut3_worker(void* arg) {
+    lut3_job* j = (lut3_job*)arg;
+    for (int64_t i = j->b; i < j->e; ++i) {
+        uint32_t k = j->keys[i];
+        j->out[i] = or_lut3_entry(j->gs, j->ws, j->hs, k & 0xFF, (k >> 8) & 0xFF, (k >> 16) & 0xFF);
+    }
+    return NULL;
+}
+
+/* or_lut3_entry for a list of keys k = g0 | g1<<8 | g2<<16 (threads split the list). */
+void or_lut3_entries(const uint8_t* gs, int32_t ws, int32_t hs, const uint32_t* keys, int64_t n,
+                     uint32_t* out, int32_t nthreads) {
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    lut3_job jobs[256];
+    for (int32_t i = 0; i < nthreads; ++i) {
+        lut3_job j = {gs, ws, hs, keys, out, n * i / nthreads, n * (i + 1) / nthreads};
+        jobs[i] = j;
+    }
+    if (nthreads == 1) { lut3_worker(&jobs[0]); return; }
+    for (int32_t i = 0; i < nthreads; ++i) pthread_create(&th[i], NULL, lut3_worker, &jobs[i]);
+    for (int32_t i = 0; i < nthreads; ++i) pthread_join(th[i], NULL);
+}
+
 typedef struct {
     const uint8_t* gs; int32_t ws, hs; uint32_t* lut; int32_t k_begin, k_end;
 } lut_job;
@@ -144,8 +190,13 @@ void or_build_lut(const uint8_t* gs, int32_t ws, int32_t hs, uint32_t* lut, int3
 /* ------------------------------------------------------------------------------------ */
 static int32_t clampi(int32_t v, int32_t lo, int32_t hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
-/* LUT key of a guide value: channels 0 and 1 (R11). */
-static uint32_t lut_at(const uint32_t* lut, const uint8_t* g) { return lut[(uint32_t)g[0] | ((uint32_t)g[1] << 8)]; }
+/* u* for a guide value: the table entry of channels 0 and 1 (R11), or with lut_rgb the exact
+ * three-channel search (R26), evaluated directly. */
+static uint32_t lut_at(const or_params* prm, const uint32_t* lut, const uint8_t* gs, int32_t ws, int32_t hs,
+                       const uint8_t* g) {
+    if (prm->lut_rgb) return or_lut3_entry(gs, ws, hs, g[0], g[1], g[2]);
+    return lut[(uint32_t)g[0] | ((uint32_t)g[1] << 8)];
+}
 
 void or_stylize_pixel(const or_params* prm, const uint8_t* gs, int32_t ws, int32_t hs,
                       const uint32_t* lut, const uint8_t* gt, int32_t wt, int32_t ht,
@@ -156,7 +207,7 @@ void or_stylize_pixel(const or_params* prm, const uint8_t* gs, int32_t ws, int32
         or_nearest_seed(px, py, l, prm->seed, prm->zero_jitter, &qx, &qy); /* line 382 */
         qx = clampi(qx, 0, wt - 1);                                        /* R8 */
         qy = clampi(qy, 0, ht - 1);
-        uint32_t u = lut_at(lut, gt + 4 * ((int64_t)qy * wt + qx));        /* line 383 */
+        uint32_t u = lut_at(prm, lut, gs, ws, hs, gt + 4 * ((int64_t)qy * wt + qx)); /* line 383 */
         int32_t ux = (int32_t)(u & 0xFFFFu), uy = (int32_t)(u >> 16);
         int32_t sx = ux + (px - qx), sy = uy + (py - qy);                  /* u* + (p - q_l) */
         if (sx < 0 || sx >= ws || sy < 0 || sy >= hs) continue;           /* R9 */
@@ -176,7 +227,7 @@ void or_stylize_pixel(const or_params* prm, const uint8_t* gs, int32_t ws, int32
             return;                                                        /* line 388 */
         }
     }
-    *coord = lut_at(lut, gt_p);                                            /* R12 */
+    *coord = lut_at(prm, lut, gs, ws, hs, gt_p);                           /* R12 */
     *level = 0;
 }
 

@@ -31,6 +31,7 @@ typedef struct {
     int32_t  zero_jitter;     /* 1: RandomJitterTable == 0 everywhere (test hook)              */
     int32_t  w[4];            /* per-channel weights of e^2 (SPEC compose_guides)   */
     int32_t  label_channel;   /* -1: none; else a segmentation label byte   */
+    int32_t  lut_rgb;         /* 1: u* by exact search over channels 0..2 (R26), lut unused    */
 } or_params;
 
 /* R5 / SURVEY App. A: the stateless hash that realises RandomJitterTable. */
@@ -57,6 +58,13 @@ uint32_t or_lut_entry(const uint8_t* gs, int32_t ws, int32_t hs, int32_t g0, int
 /* The full 256x256 table, LUT[g0 | g1<<8].  nthreads>1 splits the KEYS over threads;
  * every entry is still computed by or_lut_entry. */
 void or_build_lut(const uint8_t* gs, int32_t ws, int32_t hs, uint32_t* lut, int32_t nthreads);
+
+/* Exact three-channel guide search ("or a tree search", reading R26):
+ * u* = argmin_u over channels 0,1,2, ties -> smallest row-major index.  x | y<<16. */
+uint32_t or_lut3_entry(const uint8_t* gs, int32_t ws, int32_t hs, int32_t g0, int32_t g1, int32_t g2);
+/* or_lut3_entry for n keys g0 | g1<<8 | g2<<16 (nthreads split the list). */
+void or_lut3_entries(const uint8_t* gs, int32_t ws, int32_t hs, const uint32_t* keys, int64_t n,
+                     uint32_t* out, int32_t nthreads);
 
 /* Alg. 2 ParallelStyleBlit for one target pixel with the fallback of
  * R12.  Writes the source coordinate (x | y<<16) and the accepting level (0 = fallback). */

@@ -504,3 +504,85 @@ def test_segmentation_never_crosses_labels():
     a = oracle.stylize(oracle.Params(t=9.0, L=4, C=4, label_channel=3), cs, gs2, lut, gt2)
     b = oracle.stylize(oracle.Params(t=9.0, L=4, C=3), cs, gs2, lut, gt2)
     assert all((x == y).all() for x, y in zip(a, b))
+
+
+# ------------------------------------------ exact 3-channel guide search (R26)
+def _numpy_lut3_bruteforce(gs, keys):
+    """Independent: vectorised 3-channel squared distances, np.argmin = first row-major min."""
+    hs, ws = gs.shape[:2]
+    g = gs[..., :3].reshape(-1, 3).astype(np.int64)
+    out = []
+    for k in keys:
+        kk = np.array([k & 0xFF, (k >> 8) & 0xFF, (k >> 16) & 0xFF], np.int64)
+        i = int(np.argmin(((g - kk) ** 2).sum(1)))
+        out.append((i % ws) | ((i // ws) << 16))
+    return np.array(out, np.uint32)
+
+
+@pytest.mark.parametrize("ws,hs,vmax", [(7, 5, 256), (16, 16, 4), (24, 20, 256), (9, 31, 2)])
+def test_lut3_bruteforce_tiny(ws, hs, vmax):
+    rng = np.random.RandomState(ws * 31 + hs)
+    gs = rng.randint(0, vmax, (hs, ws, 4)).astype(np.uint8)
+    keys = rng.randint(0, 1 << 24, 500).astype(np.uint32)
+    keys = np.concatenate([keys, np.array([0, 0xFFFFFF, 0x00FF00, 0xFF00FF], np.uint32)])
+    ref = _numpy_lut3_bruteforce(gs, keys)
+    assert (oracle.lut3_entries(gs, keys, nthreads=3) == ref).all()
+    for k, r in list(zip(keys, ref))[:40]:
+        assert oracle.lut3_entry(gs, int(k) & 0xFF, (int(k) >> 8) & 0xFF, (int(k) >> 16) & 0xFF) == r
+
+
+def test_lut3_lattice_closed_form():
+    """G_S = the 4^3 lattice {0,85,170,255}^3 (8x8 pixels, a shuffled order): the nearest
+    lattice point rounds each channel to the nearest multiple of 85 (85 is odd, so no integer
+    key is half-way: unique), and u* is where that point sits."""
+    rng = np.random.RandomState(7)
+    pts = np.array([(a, b, c) for a in range(4) for b in range(4) for c in range(4)]) * 85
+    perm = rng.permutation(64)
+    gs = np.zeros((8, 8, 4), np.uint8)
+    gs[..., :3] = pts[perm].reshape(8, 8, 3)
+    gs[..., 3] = rng.randint(0, 256, (8, 8))  # ignored
+    where = {tuple(pts[perm[i]]): i for i in range(64)}
+    keys = rng.randint(0, 1 << 24, 2000).astype(np.uint32)
+    got = oracle.lut3_entries(gs, keys)
+    for k, u in zip(keys, got):
+        g = np.array([k & 0xFF, (k >> 8) & 0xFF, (k >> 16) & 0xFF])
+        i = where[tuple((np.floor(g / 85.0 + 0.5) * 85).astype(int))]
+        assert u == ((i % 8) | ((i // 8) << 16))
+
+
+def test_lut3_reduces_to_lut_when_channel2_constant():
+    """A constant channel 2 adds the same (k2 - c)^2 to every pixel: same argmin, same tie
+    rule, so the 3-channel search equals the 2-channel table for every k2."""
+    rng = np.random.RandomState(11)
+    gs = rng.randint(0, 6, (12, 14, 4)).astype(np.uint8) * 40
+    gs[..., 2] = 93
+    lut = oracle.build_lut(gs)
+    keys = rng.randint(0, 1 << 24, 3000).astype(np.uint32)
+    assert (oracle.lut3_entries(gs, keys) == lut[keys & 0xFFFF]).all()
+
+
+def test_stylize_lut_rgb():
+    """Alg. 2 with u* from the exact 3-channel search: (a) equals the table path when channel
+    2 of G_S is constant; (b) G_T = G_S with injective RGB copies every pixel at level L even
+    where the first two channels alone are ambiguous (the 2-channel table cannot)."""
+    rng = np.random.RandomState(3)
+    W = H = 32
+    cs = synth.painted_style(W, H, seed=5).numpy()
+    gs = rng.randint(0, 256, (H, W, 4)).astype(np.uint8)
+    gs[..., 2] = 17
+    gt = rng.randint(0, 256, (H, W, 4)).astype(np.uint8)
+    lut = oracle.build_lut(gs)
+    a = oracle.stylize(oracle.Params(t=60.0, L=3, C=3), cs, gs, lut, gt)
+    b = oracle.stylize(oracle.Params(t=60.0, L=3, C=3, lut_rgb=True), cs, gs, None, gt)
+    assert all((x == y).all() for x, y in zip(a, b))
+    # (b): channels 0,1 take only 4 values (massively ambiguous), channel 2 makes RGB injective
+    gs2 = np.zeros((H, W, 4), np.uint8)
+    idx = rng.permutation(W * H).reshape(H, W)
+    gs2[..., 0] = (idx % 4) * 60
+    gs2[..., 1] = ((idx // 4) % 4) * 60
+    gs2[..., 2] = idx // 16 * 4
+    _, coords, lv = oracle.stylize(oracle.Params(t=0.5, L=3, C=3, lut_rgb=True), cs, gs2, None, gs2)
+    yy, xx = np.mgrid[0:H, 0:W]
+    assert (coords == (xx | (yy << 16))).all() and (lv == 3).all()
+    _, coords2, _ = oracle.stylize(oracle.Params(t=0.5, L=3, C=3), cs, gs2, oracle.build_lut(gs2), gs2)
+    assert (coords2 != coords).any()
