@@ -57,6 +57,9 @@ typedef enum {
 #define SB_JITTER_ZERO 0x1u  /* RandomJitterTable == 0: seeds on the regular grid (tests)  */
 #define SB_NO_COLOR    0x2u  /* compute coords/levels only; ct may be NULL                 */
 #define SB_LABEL       0x4u  /* guide byte `label_channel` is a segmentation label (below)   */
+#define SB_LUT_RGB     0x8u  /* `lut` is the exact 3-channel table of sb_build_lut3 (2^24
+                                entries, key G[0] | G[1]<<8 | G[2]<<16) instead of the
+                                2-channel table                                            */
 
 #define SB_MAX_LEVELS 12      /* level l uses spacing h = 2^l, l in [1, SB_MAX_LEVELS]       */
 #define SB_MAX_RADIUS 7       /* voting radius r in [0, SB_MAX_RADIUS]; (2r+1)^2*255 < 2^16   */
@@ -78,7 +81,7 @@ typedef struct {
     /* Jitter seed of the RandomJitterTable; frame i of a batch uses
      * frame_seeds[i] (default seed + i).                                */
     uint32_t seed;
-    uint32_t flags;       /* SB_JITTER_ZERO | SB_NO_COLOR                                  */
+    uint32_t flags;       /* SB_JITTER_ZERO | SB_NO_COLOR | SB_LABEL | SB_LUT_RGB          */
     /* Output strip [row_begin, row_end) of the target (0,0 = all rows).  Only these rows
      * of ct are written; with r > 0 the coords/level rows [row_begin - r, row_end + r)
      * (clipped) are written because the vote reads them.  Results equal the whole-frame
@@ -107,9 +110,23 @@ size_t sb_lut_workspace_bytes(void);
 sb_status sb_build_lut(const uint8_t* gs, int32_t ws, int32_t hs, uint32_t* lut,
                        void* workspace, void* stream);
 
+/* Bytes of device workspace sb_build_lut3 needs (2^24 x 8 = 128 MiB). */
+size_t sb_lut3_workspace_bytes(void);
+
+/* Exact three-channel guide search, tabulated (the look-up "or a tree
+ * search"; reading R26): lut3[k] = x | y<<16 of the source
+ * pixel u minimising sum_{c<3} (k_c - G_S[u].c)^2, k = k0 | k1<<8 | k2<<16, ties -> the
+ * smallest row-major index (the rule of R10).  Used by sb_stylize* with SB_LUT_RGB.
+ *   gs         device, ws*hs*4 bytes, the source guide G_S (channel 3 ignored)
+ *   lut3       device, 2^24 uint32 (64 MiB), output
+ *   workspace  device, sb_lut3_workspace_bytes() bytes, scratch (contents undefined after) */
+sb_status sb_build_lut3(const uint8_t* gs, int32_t ws, int32_t hs, uint32_t* lut3,
+                        void* workspace, void* stream);
+
 /* Alg. 2 for every target pixel, then the vote when prm->blend_radius > 0.
  *   cs, gs     device, ws*hs*4: style exemplar C_S and source guide G_S
- *   lut        device, 65536 uint32 from sb_build_lut(gs)
+ *   lut        device, 65536 uint32 from sb_build_lut(gs); with SB_LUT_RGB, 2^24 uint32
+ *              from sb_build_lut3(gs)
  *   gt         device, wt*ht*4: target guide G_T
  *   ct         device, wt*ht*4, output C_T (may be NULL iff SB_NO_COLOR)
  *   coords     device, wt*ht uint32, output source coordinate per pixel (the NNF,

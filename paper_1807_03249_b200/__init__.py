@@ -18,11 +18,11 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import SB_JITTER_ZERO, SB_LABEL, SB_NO_COLOR, StyleBlitError, check, lib
+from ._lib import SB_JITTER_ZERO, SB_LABEL, SB_LUT_RGB, SB_NO_COLOR, StyleBlitError, check, lib
 
 __all__ = [
-    "Params", "build_lut", "stylize", "stylize_batch", "vote", "stylize_batch_host", "launch_count",
-    "version", "SB_JITTER_ZERO", "SB_NO_COLOR", "SB_LABEL", "StyleBlitError",
+    "Params", "build_lut", "build_lut3", "stylize", "stylize_batch", "vote", "stylize_batch_host", "launch_count",
+    "version", "SB_JITTER_ZERO", "SB_NO_COLOR", "SB_LABEL", "SB_LUT_RGB", "StyleBlitError",
 ]
 
 
@@ -40,9 +40,11 @@ class Params:
     row_end: int = 0
     weights: tuple = (0, 0, 0, 0)  # per-channel integer weights; all zero = unit weights
     label_channel: int | None = None  # segmentation label byte (sets SB_LABEL)
+    lut_rgb: bool = False             # `lut` is the 2^24-entry table of build_lut3 (sets SB_LUT_RGB)
 
     def c(self) -> _lib.SbParams:
         flags = int(self.flags) | (SB_LABEL if self.label_channel is not None else 0)
+        flags |= SB_LUT_RGB if self.lut_rgb else 0
         w = (C.c_uint8 * 4)(*[int(v) for v in self.weights])
         return _lib.SbParams(float(self.threshold), int(self.levels), int(self.blend_radius),
                              int(self.guide_channels), int(self.seed) & 0xFFFFFFFF, flags,
@@ -89,6 +91,27 @@ def build_lut(gs: torch.Tensor, lut: torch.Tensor | None = None, workspace: torc
     return lut
 
 
+def build_lut3(gs: torch.Tensor, lut3: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+               stream=None) -> torch.Tensor:
+    """sb_build_lut3: the exact 3-channel guide search tabulated for all 2^24 keys
+    ("or a tree search"; R26).  64 MiB table, 128 MiB workspace."""
+    _dev(gs, "gs", torch.uint8, (3,))
+    ws, hs = _img_wh(gs, "gs")
+    if lut3 is None:
+        lut3 = torch.empty(1 << 24, dtype=torch.int32, device=gs.device)
+    _dev(lut3, "lut3", torch.int32, (1,))
+    if workspace is None:
+        workspace = torch.empty(lib().sb_lut3_workspace_bytes(), dtype=torch.uint8, device=gs.device)
+    check(lib().sb_build_lut3(gs.data_ptr(), ws, hs, lut3.data_ptr(), workspace.data_ptr(), _stream(stream)))
+    return lut3
+
+
+def _check_lut(prm: Params, lut: torch.Tensor) -> None:
+    want = (1 << 24) if prm.lut_rgb else 65536
+    if lut.numel() != want:
+        raise ValueError(f"lut has {lut.numel()} entries; {'lut_rgb' if prm.lut_rgb else '2-channel'} needs {want}")
+
+
 def _outputs(prm: Params, shape_px: tuple[int, ...], device, ct, coords, level, want_level: bool):
     no_color = bool(prm.flags & SB_NO_COLOR)
     if ct is None and not no_color:
@@ -119,6 +142,7 @@ def stylize_batch(prm: Params, cs: torch.Tensor, gs: torch.Tensor, lut: torch.Te
     _dev(cs, "cs", torch.uint8, (3,))
     _dev(gs, "gs", torch.uint8, (3,))
     _dev(lut, "lut", torch.int32, (1,))
+    _check_lut(prm, lut)
     _dev(gt, "gt", torch.uint8, (4,))
     ws, hs = _img_wh(gs, "gs")
     if _img_wh(cs, "cs") != (ws, hs):
@@ -180,6 +204,7 @@ def stylize_batch_host(prm: Params, cs: torch.Tensor, gs: torch.Tensor, lut: tor
     seeds = None
     if frame_seeds is not None:
         seeds = (C.c_uint32 * n)(*[int(s) & 0xFFFFFFFF for s in frame_seeds])
+    _check_lut(prm, lut)
     p = prm.c()
     check(lib().sb_stylize_batch_host(C.byref(p), n, seeds, _dev(cs, "cs", torch.uint8, (3,)),
                                       _dev(gs, "gs", torch.uint8, (3,)), ws, hs, _dev(lut, "lut", torch.int32, (1,)),

@@ -17,12 +17,13 @@ SB_OK, SB_EINVAL, SB_EUNSUPPORTED, SB_ECUDA = 0, 1, 2, 3
 SB_JITTER_ZERO = 0x1
 SB_NO_COLOR = 0x2
 SB_LABEL = 0x4
+SB_LUT_RGB = 0x8
 SB_MAX_LEVELS = 12
 SB_MAX_RADIUS = 7
 
 # every symbol include/styleblit.h declares
 EXPORTS = (
-    "sb_lut_workspace_bytes", "sb_build_lut", "sb_stylize", "sb_stylize_batch", "sb_vote",
+    "sb_lut_workspace_bytes", "sb_build_lut", "sb_lut3_workspace_bytes", "sb_build_lut3", "sb_stylize", "sb_stylize_batch", "sb_vote",
     "sb_host_workspace_bytes", "sb_stylize_batch_host", "sb_last_launch_count",
     "sb_last_error", "sb_version",
 )
@@ -66,6 +67,10 @@ def lib() -> C.CDLL:
     l.sb_lut_workspace_bytes.argtypes = []
     l.sb_build_lut.restype = C.c_int
     l.sb_build_lut.argtypes = [u8p, i32, i32, u32p, vp, vp]
+    l.sb_lut3_workspace_bytes.restype = C.c_size_t
+    l.sb_lut3_workspace_bytes.argtypes = []
+    l.sb_build_lut3.restype = C.c_int
+    l.sb_build_lut3.argtypes = [u8p, i32, i32, u32p, vp, vp]
     l.sb_stylize.restype = C.c_int
     l.sb_stylize.argtypes = [C.POINTER(SbParams), u8p, u8p, i32, i32, u32p, u8p, i32, i32, u8p, u32p, u8p, vp]
     l.sb_stylize_batch.restype = C.c_int

@@ -70,7 +70,7 @@ sb_status validate(const sb_params* prm, int32_t n_frames, const uint8_t* cs, co
         return fail(SB_EINVAL, "blend_radius r=%d outside [0,%d]", prm->blend_radius, SB_MAX_RADIUS);
     if (prm->guide_channels < 2 || prm->guide_channels > 4)
         return fail(SB_EINVAL, "guide_channels C=%d not in {2,3,4}", prm->guide_channels);
-    if (prm->flags & ~(SB_JITTER_ZERO | SB_NO_COLOR | SB_LABEL))
+    if (prm->flags & ~(SB_JITTER_ZERO | SB_NO_COLOR | SB_LABEL | SB_LUT_RGB))
         return fail(SB_EINVAL, "flags 0x%x has unknown bits", prm->flags);
     if ((prm->flags & SB_LABEL) && (prm->label_channel < 0 || prm->label_channel > 3))
         return fail(SB_EINVAL, "label_channel=%d outside [0,3]", prm->label_channel);
@@ -97,6 +97,7 @@ sb_status validate(const sb_params* prm, int32_t n_frames, const uint8_t* cs, co
     memset(&p, 0, sizeof(p));
     sb::StylizeArgs& a = p.s;
     a.cs = cs; a.gs = gs; a.ws = ws; a.hs = hs; a.lut = lut; a.gt = gt; a.wt = wt; a.ht = ht;
+    a.key_mask = (prm->flags & SB_LUT_RGB) ? 0xFFFFFFu : 0xFFFFu;
     a.L = prm->levels;
     const double t2 = std::ceil((double)t * (double)t);  // exact: t is a float (reading R2)
     a.T2 = t2 >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)t2;
@@ -174,6 +175,22 @@ sb_status sb_build_lut(const uint8_t* gs, int32_t ws, int32_t hs, uint32_t* lut,
         return fail(SB_EINVAL, "gs/lut/workspace must be 16-byte aligned");
     cudaError_t e = sb::launch_build_lut(gs, ws, hs, lut, workspace, (cudaStream_t)stream, &g_launches);
     if (e != cudaSuccess) return cuda_fail(e, "sb_build_lut launch");
+    return SB_OK;
+}
+
+size_t sb_lut3_workspace_bytes(void) { return ((size_t)1 << 24) * 2 * sizeof(uint32_t); }
+
+sb_status sb_build_lut3(const uint8_t* gs, int32_t ws, int32_t hs, uint32_t* lut3, void* workspace, void* stream) {
+    g_launches = 0;
+    sb_status s;
+    if (!gs) return fail(SB_EINVAL, "gs (source guide G_S) is NULL");
+    if (!lut3) return fail(SB_EINVAL, "lut3 is NULL");
+    if (!workspace) return fail(SB_EINVAL, "workspace is NULL (need sb_lut3_workspace_bytes() bytes)");
+    if ((s = check_dims("source (ws,hs)", ws, hs)) != SB_OK) return s;
+    if (!aligned16(gs) || !aligned16(workspace) || !aligned16(lut3))
+        return fail(SB_EINVAL, "gs/lut3/workspace must be 16-byte aligned");
+    cudaError_t e = sb::launch_build_lut3(gs, ws, hs, lut3, workspace, (cudaStream_t)stream, &g_launches);
+    if (e != cudaSuccess) return cuda_fail(e, "sb_build_lut3 launch");
     return SB_OK;
 }
 

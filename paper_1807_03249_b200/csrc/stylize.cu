@@ -79,7 +79,7 @@ __device__ __forceinline__ void build_one(Smem& sm, const StylizeArgs& a, const 
     cell_seed(g.cx0 + ci, g.cy0 + cj, l, c_l, a.zero_jitter != 0, sx, sy);
     const int qx = min(max(sx, 0), a.wt - 1);
     const int qy = min(max(sy, 0), a.ht - 1);
-    const uint32_t u = __ldg(a.lut + (__ldg(gtf + (uint32_t)(qy * a.wt + qx)) & 0xFFFFu));
+    const uint32_t u = __ldg(a.lut + (__ldg(gtf + (uint32_t)(qy * a.wt + qx)) & a.key_mask));
     // delta = u* - q packed as dy*65536 + dx: p_packed + delta is the packed candidate s
     const int dpack = ((int)(u >> 16) - qy) * 65536 + ((int)(u & 0xFFFFu) - qx);
     sm.cell[g.off + ci * CS + cj] = make_int4(32 * (sx - x0), 32 * (sy - y0), dpack, 0);
@@ -255,7 +255,7 @@ __device__ __forceinline__ uint32_t direct_candidate(const StylizeArgs& a, const
         }
     qx = min(max(qx, 0), a.wt - 1);
     qy = min(max(qy, 0), a.ht - 1);
-    const uint32_t u = __ldg(a.lut + (__ldg(gtf + (uint32_t)(qy * a.wt + qx)) & 0xFFFFu));
+    const uint32_t u = __ldg(a.lut + (__ldg(gtf + (uint32_t)(qy * a.wt + qx)) & a.key_mask));
     const int sx = (int)(u & 0xFFFFu) + (px - qx);
     const int sy = (int)(u >> 16) + (py - qy);
     return (uint32_t)(sy * 65536 + sx);
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
             const int idx = q[k];
             const int rx = idx & (TW - 1), ry = idx / TW;
             const uint32_t gp = __ldg(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + rx));
-            sm.coord[idx] = __ldg(a.lut + (gp & 0xFFFFu));
+            sm.coord[idx] = __ldg(a.lut + (gp & a.key_mask));
             if (want_lvl) lvl[idx] = 0;
         }
     }

@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(256) stylize_naive_kernel(const __grid_constan
             }
         qx = min(max(qx, 0), a.wt - 1);  // R8
         qy = min(max(qy, 0), a.ht - 1);
-        const uint32_t u = __ldg(a.lut + (__ldg(gt + (int64_t)qy * a.wt + qx) & 0xFFFFu));
+        const uint32_t u = __ldg(a.lut + (__ldg(gt + (int64_t)qy * a.wt + qx) & a.key_mask));
         const int sx = (int)(u & 0xFFFFu) + (px - qx);
         const int sy = (int)(u >> 16) + (py - qy);
         if ((unsigned)sx >= (unsigned)a.ws || (unsigned)sy >= (unsigned)a.hs) continue;  // R9
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256) stylize_naive_kernel(const __grid_constan
         const bool ok = EXT ? guide_ok_ext(gp, g, a.cmask, a.w, a.lmask, a.T2) : guide_d2(gp, g, a.cmask) < a.T2;
         if (ok) { coord = pack_xy(sx, sy); level = l; break; }
     }
-    if (level == 0) coord = __ldg(a.lut + (gp & 0xFFFFu));  // R12
+    if (level == 0) coord = __ldg(a.lut + (gp & a.key_mask));  // R12
     const int64_t o = fpx * frame + (int64_t)py * a.wt + px;
     if (a.coords) a.coords[o] = coord;
     if (a.level) a.level[o] = (uint8_t)level;
