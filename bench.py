@@ -52,6 +52,8 @@ def parse():
                     help="frame: each GPU stylizes its own frames (weak scaling, no collective); "
                          "strip: every frame is split into row strips across GPUs and the C_T strips "
                          "are gathered to rank 0 with NCCL each step")
+    ap.add_argument("--lut-rgb-steps", type=int, default=10,
+                    help="timed steps of the exact 3-channel guide-search run (SB_LUT_RGB, 0: skip)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -279,6 +281,37 @@ def run_ours(args):
                  "blend_radius": 2, "kernels": bl["kernels"], "gpu_launches": bl["launches"], "clocks": bl["clocks"],
                  "step": "LUT build + stylize (coords) + vote r=2"}
 
+    # ---- NEXT #3: the exact 3-channel guide search (SB_LUT_RGB, R26).  The 2^24-entry
+    #      table is built once per exemplar (timed on its own); a step = stylize with it.
+    lut_rgb = None
+    if args.lut_rgb_steps > 0 and not strip:
+        lut3 = torch.empty(1 << 24, dtype=torch.int32, device=dev)
+        ws3 = torch.empty(sb.lib().sb_lut3_workspace_bytes(), dtype=torch.uint8, device=dev)
+        sb.build_lut3(gs, lut3, ws3)
+        torch.cuda.synchronize(dev)
+        a3, b3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a3.record(stream)
+        for _ in range(3):
+            sb.build_lut3(gs, lut3, ws3)
+        b3.record(stream)
+        torch.cuda.synchronize(dev)
+        build_ms = a3.elapsed_time(b3) / 3
+        prm3 = sb.Params(threshold=cfg["t"], levels=cfg["L"], guide_channels=cfg["C"], seed=cfg["seed"], lut_rgb=True)
+        for _ in range(3):
+            sb.stylize_batch(prm3, cs, gs, lut3, gt, frame_seeds=seeds, ct=ct, coords=coords, want_level=False)
+        torch.cuda.synchronize(dev)
+        a3.record(stream)
+        for _ in range(args.lut_rgb_steps):
+            sb.stylize_batch(prm3, cs, gs, lut3, gt, frame_seeds=seeds, ct=ct, coords=coords, want_level=False)
+        b3.record(stream)
+        torch.cuda.synchronize(dev)
+        ms3 = a3.elapsed_time(b3) / args.lut_rgb_steps
+        lut_rgb = {"value": round(px_job / (ms3 * 1e-3) / 1e6, 1), "unit": "MP/s", "ms_per_step": round(ms3, 4),
+                   "lut3_build_ms": round(build_ms, 3),
+                   "step": "stylize (coords + blit colours) with the exact 3-channel table; table built once "
+                           "per exemplar (lut3_build_ms, 2^24 entries)"}
+        del lut3, ws3
+
     # ---- e2e through the host-buffer ABI call (pinned host memory, copies inside timing)
     e2e = None
     if not args.no_e2e and args.e2e_steps > 0 and not strip:
@@ -344,6 +377,7 @@ def run_ours(args):
         "clocks": main["clocks"],
         "e2e": e2e,
         "blend_r2": blend,
+        "lut_rgb": lut_rgb,
     }
     return out, rank, world
 
