@@ -97,6 +97,7 @@ def lib():
         l.or_lut3_entry.restype = C.c_uint32
         l.or_lut3_entry.argtypes = [u8p, i32, i32, i32, i32, i32]
         l.or_lut3_entries.argtypes = [u8p, i32, i32, u32p, C.c_int64, u32p, i32]
+        l.or_blit_bruteforce.argtypes = [C.POINTER(_Params), u8p, u8p, i32, i32, u32p, u8p, i32, i32, u8p, u32p, u8p]
         l.or_version.restype = C.c_char_p
         _lib = l
     return _lib
@@ -199,6 +200,19 @@ def stylize(prm: Params, cs, gs, lut, gt, nthreads: int = 1):
     p = prm.c()
     lib().or_stylize(C.byref(p), _u8(cs), _u8(gs), ws, hs, _u32(lut), _u8(gt), wt, ht,
                      _u8(ct), _u32(coords), _u8(level), nthreads)
+    return ct, coords, level
+
+
+def blit_bruteforce(prm: Params, cs, gs, lut, gt):
+    """Alg. 1: (ct, coords, level), level 1 = copied, 0 = fallback."""
+    ws, hs = _img(gs)
+    wt, ht = _img(gt)
+    ct = np.zeros((ht, wt, 4), np.uint8)
+    coords = np.zeros((ht, wt), np.uint32)
+    level = np.zeros((ht, wt), np.uint8)
+    p = prm.c()
+    lib().or_blit_bruteforce(C.byref(p), _u8(cs), _u8(gs), ws, hs, _u32(lut), _u8(gt), wt, ht,
+                             _u8(ct), _u32(coords), _u8(level))
     return ct, coords, level
 
 

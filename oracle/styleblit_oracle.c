@@ -325,3 +325,57 @@ void or_vote(const uint32_t* coords, int32_t wt, int32_t ht, const uint8_t* cs, 
     for (int32_t i = 0; i < nthreads; ++i) pthread_create(&th[i], NULL, vote_worker, &jobs[i]);
     for (int32_t i = 0; i < nthreads; ++i) pthread_join(th[i], NULL);
 }
+
+/* ------------------------------------------------------------------------------------ */
+/* Alg. 1, the brute-force sequential synthesizer, as  */
+/* a quality/statistics reference -- not a speed path.  Transcribed in the paper's order: */
+/* target pixels p row-major; for an empty p, u* = the look-up of G_T[p] (line "u* =      */
+/* argmin_u ||G_T[p] - G_S[u]||", the same look-up as Alg. 2, R11/R26); then every source */
+/* pixel q row-major: if p + (q - u*) is inside the target (reading R27) and empty, and   */
+/* e = ||G_T[p + (q - u*)] - G_S[q]|| < t, copy C_S[q] there.  Pixels left empty take the */
+/* look-up fallback (level 0, as R12).  Filled pixels get level 1.                        */
+/* ------------------------------------------------------------------------------------ */
+void or_blit_bruteforce(const or_params* prm, const uint8_t* cs, const uint8_t* gs, int32_t ws, int32_t hs,
+                        const uint32_t* lut, const uint8_t* gt, int32_t wt, int32_t ht,
+                        uint8_t* ct, uint32_t* coords, uint8_t* level) {
+    const int64_t npx = (int64_t)wt * ht;
+    uint8_t* filled = (uint8_t*)calloc((size_t)npx, 1);
+    for (int32_t py = 0; py < ht; ++py) {
+        for (int32_t px = 0; px < wt; ++px) {
+            if (filled[(int64_t)py * wt + px]) continue;                  /* "C_T[p] is empty" */
+            const uint32_t u = lut_at(prm, lut, gs, ws, hs, gt + 4 * ((int64_t)py * wt + px));
+            const int32_t ux = (int32_t)(u & 0xFFFFu), uy = (int32_t)(u >> 16);
+            for (int32_t qy = 0; qy < hs; ++qy) {
+                for (int32_t qx = 0; qx < ws; ++qx) {                     /* each q in C_S */
+                    const int32_t tx = px + (qx - ux), ty = py + (qy - uy);
+                    if (tx < 0 || tx >= wt || ty < 0 || ty >= ht) continue;  /* R27 */
+                    const int64_t ti = (int64_t)ty * wt + tx;
+                    if (filled[ti]) continue;
+                    const uint8_t* gt_t = gt + 4 * ti;
+                    const uint8_t* gs_q = gs + 4 * ((int64_t)qy * ws + qx);
+                    if (prm->label_channel >= 0 && gt_t[prm->label_channel] != gs_q[prm->label_channel]) continue;
+                    double e2 = 0.0;
+                    for (int32_t c = 0; c < prm->C; ++c) {
+                        if (c == prm->label_channel) continue;
+                        double d = (double)gt_t[c] - (double)gs_q[c];
+                        e2 += (double)prm->w[c] * d * d;
+                    }
+                    if (sqrt(e2) < prm->t) {                               /* e < t */
+                        filled[ti] = 1;
+                        coords[ti] = (uint32_t)qx | ((uint32_t)qy << 16);
+                        if (level) level[ti] = 1;
+                        if (ct) memcpy(ct + 4 * ti, cs + 4 * ((int64_t)qy * ws + qx), 4);
+                    }
+                }
+            }
+        }
+    }
+    for (int64_t i = 0; i < npx; ++i) {                                    /* never filled */
+        if (filled[i]) continue;
+        const uint32_t u = lut_at(prm, lut, gs, ws, hs, gt + 4 * i);
+        coords[i] = u;
+        if (level) level[i] = 0;
+        if (ct) memcpy(ct + 4 * i, cs + 4 * ((int64_t)(u >> 16) * ws + (u & 0xFFFFu)), 4);
+    }
+    free(filled);
+}

@@ -82,6 +82,12 @@ void or_stylize(const or_params* prm, const uint8_t* cs, const uint8_t* gs, int3
 void or_vote(const uint32_t* coords, int32_t wt, int32_t ht, const uint8_t* cs, int32_t ws,
              int32_t hs, int32_t r, uint8_t* ct, int32_t nthreads);
 
+/* Alg. 1, the brute-force sequential synthesizer, a statistics reference
+ * (SURVEY 8(f) #4).  coords/ct/level as or_stylize; level 1 = copied, 0 = look-up fallback. */
+void or_blit_bruteforce(const or_params* prm, const uint8_t* cs, const uint8_t* gs, int32_t ws, int32_t hs,
+                        const uint32_t* lut, const uint8_t* gt, int32_t wt, int32_t ht,
+                        uint8_t* ct, uint32_t* coords, uint8_t* level);
+
 const char* or_version(void);
 
 #ifdef __cplusplus
