@@ -7,7 +7,7 @@ shift
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q "$@" > gpurun_out/pytest_${TAG}.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_${TAG}.log
 timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${TAG}.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_${TAG}.log
-C="python bench.py --steps 1 --warmup 1 --blend-steps 1 --frames 16 --no-e2e --no-cpu-baseline"
+C="python bench.py --steps 1 --warmup 1 --blend-steps 1 --lut-rgb-steps 0 --frames 16 --no-e2e --no-cpu-baseline"
 if [ -n "$NCU" ]; then
   timeout 200 $C > gpurun_out/plain_${TAG}.log 2>&1 && \
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"stylize_tiled|vote_kernel" -s 1 -c 3 -o gpurun_out/prof_${TAG} $C > gpurun_out/ncu_${TAG}.log 2>&1
