@@ -320,11 +320,12 @@ def run_ours(args):
         ct_h = torch.empty_like(gt_h).pin_memory()
         prm_e = sb.Params(threshold=cfg["t"], levels=cfg["L"], blend_radius=r, guide_channels=cfg["C"],
                           seed=cfg["seed"])
-        ws_e = sb.host_workspace(WT, HT, r, 2, device=dev)
+        depth = int(os.environ.get("SB_E2E_DEPTH", "2"))
+        ws_e = sb.host_workspace(WT, HT, r, depth, device=dev)
 
         def e2e_step():
             sb.build_lut(gs, lut, lut_ws)
-            sb.stylize_batch_host(prm_e, cs, gs, lut, gt_h, ct_h, frame_seeds=seeds[:Be], workspace=ws_e, depth=2)
+            sb.stylize_batch_host(prm_e, cs, gs, lut, gt_h, ct_h, frame_seeds=seeds[:Be], workspace=ws_e, depth=depth)
 
         e2e_step()
         torch.cuda.synchronize(dev)
@@ -344,7 +345,7 @@ def run_ours(args):
         e2e = {"value": round(world * Be * WT * HT / (ems * 1e-3) / 1e6, 1), "unit": "MP/s",
                "h2d_bytes_per_step": Be * WT * HT * 4, "d2h_bytes_per_step": Be * WT * HT * 4,
                "frames_per_step": Be, "ms_per_step": round(ems, 3),
-               "api": "sb_stylize_batch_host (pinned host G_T in, pinned host C_T out, 2-deep copy/compute pipeline)"}
+               "api": f"sb_stylize_batch_host (pinned host G_T in, pinned host C_T out, {depth}-deep copy/compute pipeline)"}
 
     # ---- parity spot check of this run's outputs (sampled pixels of frame 0 vs oracle) is in tests/.
     out = {
