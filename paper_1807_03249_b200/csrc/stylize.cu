@@ -263,7 +263,7 @@ __device__ __forceinline__ uint32_t direct_candidate(const StylizeArgs& a, const
 
 }  // namespace
 
-template <bool EXT>
+template <bool EXT, bool LVL>
 __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_constant__ StylizeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -284,7 +284,6 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
     const bool colok = x0 + rx0 < a.wt;     // wt % 4 == 0: a group is all in or all out
     const int rows_here = min(TH, a.row_end - y0);
     const int L = a.L;
-    const bool want_lvl = a.level != nullptr;
     // tile row of this warp's j-th row, and whether its group exists
     auto row_of = [&](int j) { return warp + NW * j; };
     auto ok_of = [&](int j) { return colok && row_of(j) < rows_here; };
@@ -334,7 +333,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                 const int ry = row_of(j - 1);
                 const uint32_t acc = group_test<EXT>(a, pgp, pgv, pinb);
                 *reinterpret_cast<uint4*>(&sm.coord[ry * TW + rx0]) = make_uint4(pcand[0], pcand[1], pcand[2], pcand[3]);
-                if (want_lvl) *reinterpret_cast<uint32_t*>(&lvl[ry * TW + rx0]) = 0x01010101u * (uint32_t)L;
+                if (LVL) *reinterpret_cast<uint32_t*>(&lvl[ry * TW + rx0]) = 0x01010101u * (uint32_t)L;
                 rej |= (~acc & 0xFu) << (4 * (j - 1));
             }
             if (j < RPW) {
@@ -348,32 +347,34 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                 pok = ok;
             }
         }
-        if (t1) {
-            // ---- level L-1 on the warp's groups that still have a rejected pixel ----
-            uint16_t* gl = sm.glist[warp];
-            int ng = 0;
+        // ---- the warp's groups that still have a rejected pixel: lane | j<<5 | mask<<8
+        uint16_t* gl = sm.glist[warp];
+        int ng = 0;
 #pragma unroll
-            for (int j = 0; j < RPW; ++j) {
-                const uint32_t m = (rej >> (4 * j)) & 0xFu;
-                const unsigned b = __ballot_sync(0xFFFFFFFFu, m != 0);
-                if (m) gl[ng + __popc(b & lt_mask)] = (uint16_t)(lane | (j << 5) | (m << 8));
-                ng += __popc(b);
-            }
-            __syncwarp();
-            const int l1 = L - 1;
+        for (int j = 0; j < RPW; ++j) {
+            const uint32_t m = (rej >> (4 * j)) & 0xFu;
+            const unsigned b = __ballot_sync(0xFFFFFFFFu, m != 0);
+            if (m) gl[ng + __popc(b & lt_mask)] = (uint16_t)(lane | (j << 5) | (m << 8));
+            ng += __popc(b);
+        }
+        __syncwarp();
+        // One tabled level (h >= 4) on the listed groups, densely; the list is compacted in
+        // place to the groups that still have a rejected pixel (entry k is rewritten only at
+        // an index <= k, after the ballot that follows every read of its batch).
+        auto group_pass = [&](int lp, const CellGrid& g) {
+            int nn = 0;
             for (int k0 = 0; k0 < ng; k0 += 32) {
                 const int k = k0 + lane;
-                uint32_t still = 0;
-                int pbase = 0;
+                uint32_t still = 0, e = 0;
                 if (k < ng) {
-                    const uint32_t e = gl[k];
+                    e = gl[k];
                     const int grx0 = (int)(e & 31u) * 4;
                     const int ry = row_of((int)((e >> 5) & 7u));
                     const uint32_t m = e >> 8;
-                    pbase = ry * TW + grx0;
+                    const int pbase = ry * TW + grx0;
                     const uint4 gp4 = *reinterpret_cast<const uint4*>(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + grx0));
                     uint32_t cand[4];
-                    const uint32_t acc = group_eval<EXT>(sm, a, gs, gL1, l1, x0, y0, grx0, ry, gp4, cand);
+                    const uint32_t acc = group_eval<EXT>(sm, a, gs, g, lp, x0, y0, grx0, ry, gp4, cand);
                     // merge the newly accepted pixels into the group's coords: one 16-byte
                     // read-modify-write instead of four conflicting scalar stores
                     const uint32_t take = m & acc;
@@ -383,33 +384,45 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                     cv.z = (take & 4u) ? cand[2] : cv.z;
                     cv.w = (take & 8u) ? cand[3] : cv.w;
                     *reinterpret_cast<uint4*>(&sm.coord[pbase]) = cv;
-                    if (want_lvl) {
+                    if (LVL) {
 #pragma unroll
                         for (int i = 0; i < 4; ++i)
-                            if ((take >> i) & 1u) lvl[pbase + i] = (uint8_t)l1;
+                            if ((take >> i) & 1u) lvl[pbase + i] = (uint8_t)lp;
                     }
                     still = m & ~acc;
                 }
-                int tot;
-                int pos = n + warp_excl_scan(__popc(still), &tot);
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if ((still >> i) & 1u) q[pos++] = (uint16_t)(pbase + i);
-                n += tot;
+                const unsigned b = __ballot_sync(0xFFFFFFFFu, still != 0);
+                if (still) gl[nn + __popc(b & lt_mask)] = (uint16_t)((e & 0xFFu) | (still << 8));
+                nn += __popc(b);
             }
+            __syncwarp();
+            ng = nn;
+        };
+        l = L - 1;
+        if (t1) {
+            group_pass(L - 1, gL1);  // level L-1 on the groups with a rejected pixel
             l = L - 2;
-        } else {
-            // L == 2: the rejected pixels go straight to the per-pixel levels
-            int tot;
-            int pos = warp_excl_scan(__popc(rej), &tot);
-            for (int j = 0; j < RPW; ++j) {
-                const int ry = row_of(j);
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if ((rej >> (4 * j + i)) & 1u) q[pos++] = (uint16_t)(ry * TW + rx0 + i);
+            if (t2) {
+                group_pass(L - 2, gL2);
+                l = L - 3;
             }
-            n = tot;
-            l = L - 1;
+        }
+        // the pixels still rejected go to the per-pixel levels
+        for (int k0 = 0; k0 < ng; k0 += 32) {
+            const int k = k0 + lane;
+            uint32_t still = 0;
+            int pbase = 0;
+            if (k < ng) {
+                const uint32_t e = gl[k];
+                pbase = row_of((int)((e >> 5) & 7u)) * TW + (int)(e & 31u) * 4;
+                still = e >> 8;
+            }
+            int tot;
+            int pos = n + warp_excl_scan(__popc(still), &tot);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if ((still >> i) & 1u) q[pos++] = (uint16_t)(pbase + i);
+            n += tot;
         }
     } else {
         // L == 1: every valid pixel starts in the pixel queue
@@ -444,7 +457,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                 const uint32_t gp = __ldg(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + rx));
                 if (accept<EXT>(a, gs, gp, cand)) {
                     sm.coord[idx] = cand;
-                    if (want_lvl) lvl[idx] = (uint8_t)l;
+                    if (LVL) lvl[idx] = (uint8_t)l;
                 } else {
                     rej = true;
                 }
@@ -464,7 +477,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
             const int rx = idx & (TW - 1), ry = idx / TW;
             const uint32_t gp = __ldg(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + rx));
             sm.coord[idx] = __ldg(a.lut + (gp & a.key_mask));
-            if (want_lvl) lvl[idx] = 0;
+            if (LVL) lvl[idx] = 0;
         }
     }
     __syncwarp();
@@ -495,7 +508,8 @@ cudaError_t launch_stylize_tiled(const StylizeArgs& a, int n_frames, cudaStream_
     static_assert(sizeof(Smem) + TP <= 48 * 1024, "smem");
     // the level map only when requested: without it 4 CTAs leave ~92 KB of L1 per SM
     const size_t smem = sizeof(Smem) + (a.level ? TP : 0);
-    auto kern = a.ext ? stylize_tiled_kernel<true> : stylize_tiled_kernel<false>;
+    auto kern = a.ext ? (a.level ? stylize_tiled_kernel<true, true> : stylize_tiled_kernel<true, false>)
+                      : (a.level ? stylize_tiled_kernel<false, true> : stylize_tiled_kernel<false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     static const int carve = [] {
