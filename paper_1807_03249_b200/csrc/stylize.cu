@@ -111,13 +111,27 @@ __device__ __forceinline__ int warp_excl_scan(int v, int* total) {
 // Candidate test of Alg. 2 lines 384-385 on the packed candidate c = s.x | s.y<<16:
 // s inside the source (R9; a negative component borrows into a field >= 0x8000 > 32767)
 // and D = ||G_T[p] - G_S[s]||^2 < T2.  Branch-free: an outside candidate reads G_S[0].
+// G_S gather for the packed candidate c = s.x | s.y<<16 (Alg. 2).  *in: s inside the
+// source (R9; a negative component borrows into a field >= 0x8000 > 32767), tested with one
+// packed 16-bit min against (ws-1 | (hs-1)<<16); the index y*ws + x = c + y*(ws - 65536)
+// (mod 2^32); an outside candidate reads G_S[0].  Branch-free.
+__device__ __forceinline__ uint32_t gather_gs(const StylizeArgs& a, const uint32_t* __restrict__ gs, uint32_t c,
+                                              bool* in) {
+    const uint32_t lim = ((uint32_t)(a.hs - 1) << 16) | (uint32_t)(a.ws - 1);
+    uint32_t mn;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(mn) : "r"(c), "r"(lim));
+    *in = mn == c;
+    const uint32_t gi = *in ? c + (c >> 16) * (uint32_t)(a.ws - 65536) : 0u;
+    const uint32_t* p;
+    asm("mad.wide.u32 %0, %1, 4, %2;" : "=l"(p) : "r"(gi), "l"(gs));
+    return __ldg(p);
+}
+
 template <bool EXT>
 __device__ __forceinline__ bool accept(const StylizeArgs& a, const uint32_t* __restrict__ gs, uint32_t gp,
                                        uint32_t c) {
-    const uint32_t x = c & 0xFFFFu, y = c >> 16;
-    const bool inb = (x < (uint32_t)a.ws) & (y < (uint32_t)a.hs);
-    const uint32_t gi = inb ? y * (uint32_t)a.ws + x : 0u;
-    const uint32_t g = __ldg(gs + gi);
+    bool inb;
+    const uint32_t g = gather_gs(a, gs, c, &inb);
     if (EXT) return inb & guide_ok_ext(gp, g, a.cmask, a.w, a.lmask, a.T2);
     return inb & (guide_d2(gp, g, a.cmask) < a.T2);
 }
@@ -194,9 +208,8 @@ __device__ __forceinline__ uint32_t group_issue(const Smem& sm, const StylizeArg
     for (int i = 0; i < 4; ++i) {
         const uint32_t c = p0 + (uint32_t)i + winner_delta(cb, keys[i]);
         cand[i] = c;
-        const uint32_t x = c & 0xFFFFu, y = c >> 16;
-        const bool in = (x < (uint32_t)a.ws) & (y < (uint32_t)a.hs);
-        gv[i] = __ldg(gs + (in ? y * (uint32_t)a.ws + x : 0u));
+        bool in;
+        gv[i] = gather_gs(a, gs, c, &in);
         inb |= (uint32_t)in << i;
     }
     return inb;
