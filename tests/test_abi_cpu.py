@@ -49,6 +49,7 @@ def test_sm100a_cubin_present(lib):
 def test_version_and_workspace(lib):
     assert b"sm_100a" in lib.sb_version()
     assert lib.sb_lut_workspace_bytes() == 65536 * 4
+    assert lib.sb_lut3_workspace_bytes() == (1 << 24) * 8
     assert lib.sb_host_workspace_bytes(3840, 2160, 0, 2) >= 2 * 3 * 3840 * 2160 * 4
     assert lib.sb_host_workspace_bytes(0, 10, 0, 2) == 0
 
@@ -117,6 +118,15 @@ def test_build_lut_invalid(lib):
     assert lib.sb_build_lut(FAKE, 4, 4, FAKE, 0, None) == _lib.SB_EINVAL
     assert "workspace" in lib.sb_last_error().decode()
     assert lib.sb_build_lut(FAKE, 0, 4, FAKE, FAKE, None) == _lib.SB_EINVAL
+
+
+def test_build_lut3_invalid(lib):
+    assert lib.sb_build_lut3(0, 4, 4, FAKE, FAKE, None) == _lib.SB_EINVAL
+    assert "gs" in lib.sb_last_error().decode()
+    assert lib.sb_build_lut3(FAKE, 4, 4, 0, FAKE, None) == _lib.SB_EINVAL
+    assert lib.sb_build_lut3(FAKE, 4, 4, FAKE, 0, None) == _lib.SB_EINVAL
+    assert "sb_lut3_workspace_bytes" in lib.sb_last_error().decode()
+    assert lib.sb_build_lut3(FAKE, 4, 40000, FAKE, FAKE, None) == _lib.SB_EINVAL
 
 
 def test_host_batch_invalid(lib):
