@@ -315,7 +315,9 @@ def run_ours(args):
     # ---- e2e through the host-buffer ABI call (pinned host memory, copies inside timing)
     e2e = None
     if not args.no_e2e and args.e2e_steps > 0 and not strip:
-        Be = min(B, 16)
+        # the step's whole batch through host memory (fill/drain of the copy pipeline amortised
+        # over the batch); SB_E2E_FRAMES caps it (pinned host memory: 2 x 33 MB per frame)
+        Be = min(B, int(os.environ.get("SB_E2E_FRAMES", "64")))
         gt_h = gt[:Be].cpu().pin_memory()
         ct_h = torch.empty_like(gt_h).pin_memory()
         prm_e = sb.Params(threshold=cfg["t"], levels=cfg["L"], blend_radius=r, guide_channels=cfg["C"],
