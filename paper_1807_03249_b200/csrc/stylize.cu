@@ -4,7 +4,7 @@
 // threads; warp w owns tile rows w, w+8, w+16, w+24 and a thread owns 4 consecutive pixels of
 // each (uint4 I/O).  Per tile and level l the seed cells that any tile pixel can reach (its
 // 3x3 neighbourhood) are materialised in shared memory:
-//     cell = (4*(s.x - x0), 4*(s.y - y0), delta),  delta = u* - q packed as dy*65536 + dx,
+//     cell = (32*(s.x - x0), 32*(s.y - y0), delta),  delta = u* - q packed as dy*65536 + dx,
 // where s is the jittered seed (SeedPoint, lines 354-358), q = clamp(s) (reading R8) and
 // u* = LUT[G_T[q]] (line 383).  A pixel's candidate is then s = p + delta of its nearest seed
 // (line 384), so per pixel and level the work is 9 shared-memory distance evaluations, one
@@ -12,9 +12,10 @@
 //
 // Levels run coarse to fine with compaction:
 //   level L    every 4-pixel group (the pixels of a 4-aligned group share their cell for
-//              h >= 4, so the 9 seed loads and the dy terms are shared by 4 pixels);
-//   level L-1  only the groups with a rejected pixel, densely from a warp-local group list,
-//              same shared-cell evaluation;
+//              h >= 4, so the 9 seed loads and the dy terms are shared by 4 pixels),
+//              software-pipelined over the thread's 4 rows;
+//   L-1, L-2   only the groups with a rejected pixel, densely from a warp-local group list
+//              compacted in place, same shared-cell evaluation;
 //   below      the remaining pixels from a warp-local pixel queue, one per lane.
 // The tables of the levels L, L-1, L-2 that have h >= 4 are built together up front, behind
 // the kernel's only CTA barrier; afterwards each warp works on its own rows with warp-local
@@ -22,9 +23,8 @@
 // without a table (h = 2, or below L-2) evaluate their 9 seeds straight from the hash.  Pixels
 // left after level 1 take the level-0 look-up (reading R12).
 //
-// NearestSeed ties: key = 16*d + i, i = 3*(x+1) + (y+1) in Alg. 2's loop order (x outer, y
-// inner), so the minimum key is the first strict minimum (reading R7).  d < 8 h^2 keeps the
-// key in 32 bits for h <= 2^12.
+// NearestSeed ties: see code_of() -- the key 1024 d + code orders by d, then by Alg. 2's loop
+// order (x outer, y inner), so the minimum key is the first strict minimum (reading R7).
 #include <cstdlib>
 
 #include "sb_kernels.cuh"
