@@ -353,3 +353,48 @@ def test_weighted_and_segmentation_parity(case):
         sx, sy = o[1] & 0xFFFF, o[1] >> 16
         acc = o[2] > 0
         assert (gs.numpy()[sy, sx, 3][acc] == gt.numpy()[..., 3][acc]).all()
+
+
+# ------------------------------------------------------------------ CUDA graph capture
+def test_cuda_graph_capture_replay():
+    """The ABI calls only enqueue work on the caller's stream (no allocation, no sync), so a
+    whole step (LUT + stylize + vote) can be captured into a CUDA graph and replayed: replays
+    reproduce the eager result bit for bit, and follow new inputs written into the same buffers."""
+    cfg = synth.CONFIGS[2]
+    cs, gs = (t.to(DEV) for t in synth.exemplar(cfg))
+    gt = synth.target(2).to(DEV).unsqueeze(0).repeat(3, 1, 1, 1).contiguous()
+    gt[1] = torch.flip(gt[1], dims=[1])
+    prm = sb.Params(threshold=cfg["t"], levels=cfg["L"], blend_radius=2, guide_channels=cfg["C"], seed=cfg["seed"])
+    lut = torch.empty(65536, dtype=torch.int32, device=DEV)
+    lws = torch.empty(sb.lib().sb_lut_workspace_bytes(), dtype=torch.uint8, device=DEV)
+    ct = torch.empty_like(gt)
+    co = torch.empty(gt.shape[:3], dtype=torch.int32, device=DEV)
+
+    def step():
+        sb.build_lut(gs, lut, lws)
+        sb.stylize_batch(prm, cs, gs, lut, gt, ct=ct, coords=co, want_level=False)
+
+    step()
+    torch.cuda.synchronize()
+    eager_ct, eager_co = ct.clone(), co.clone()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()  # warm-up on the side stream (kernel attributes set outside capture)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    ct.zero_()
+    co.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(ct, eager_ct) and torch.equal(co, eager_co)
+    gt.copy_(torch.flip(gt, dims=[2]))  # new inputs, same buffers
+    g.replay()
+    torch.cuda.synchronize()
+    ref_ct = ct.clone()
+    step()
+    torch.cuda.synchronize()
+    assert torch.equal(ct, ref_ct) and not torch.equal(ref_ct, eager_ct)
