@@ -398,3 +398,22 @@ def test_cuda_graph_capture_replay():
     step()
     torch.cuda.synchronize()
     assert torch.equal(ct, ref_ct) and not torch.equal(ref_ct, eager_ct)
+
+
+def test_batch_longer_than_one_launch():
+    """More frames than one launch carries seeds for (512): the library splits the batch into
+    launches; every frame keeps its own seed (checked against the oracle on a sample)."""
+    n = 1100
+    cfg = synth.CONFIGS[1]
+    cs, gs = synth.exemplar(cfg)
+    frames = torch.stack([synth.heightfield_normals(16, 12, seed=9, frame=i % 7) for i in range(n)])
+    seeds = [(0x1234567 * i + 99) & 0xFFFFFFFF for i in range(n)]
+    prm = sb.Params(threshold=cfg["t"], levels=3, guide_channels=3)
+    gsd = gs.to(DEV)
+    ct, co, lv = sb.stylize_batch(prm, cs.to(DEV), gsd, sb.build_lut(gsd), frames.to(DEV), frame_seeds=seeds)
+    torch.cuda.synchronize()
+    lut = oracle_lut(gs.numpy())
+    for i in (0, 511, 512, 513, 1023, 1024, n - 1):
+        o = oracle.stylize(oracle.Params(t=cfg["t"], L=3, C=3, seed=seeds[i]), cs.numpy(), gs.numpy(), lut,
+                           frames[i].numpy())
+        assert (u32(co[i]) == o[1]).all() and (lv[i].cpu().numpy() == o[2]).all(), i
