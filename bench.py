@@ -52,6 +52,10 @@ def parse():
                     help="frame: each GPU stylizes its own frames (weak scaling, no collective); "
                          "strip: every frame is split into row strips across GPUs and the C_T strips "
                          "are gathered to rank 0 with NCCL each step")
+    ap.add_argument("--gather", default="nccl", choices=["nccl", "p2p"],
+                    help="strip mode: nccl = one NCCL gather of the C_T strips after the compute; p2p = rank 0's "
+                         "C_T buffer is mapped into every rank (CUDA IPC) and the kernels store their rows into it "
+                         "over NVLink/NVSwitch, then a one-element all-reduce orders rank 0 after the writers")
     ap.add_argument("--lut-rgb-steps", type=int, default=10,
                     help="timed steps of the exact 3-channel guide-search run (SB_LUT_RGB, 0: skip)")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -177,6 +181,10 @@ def run_ours(args):
     lut = torch.empty(65536, dtype=torch.int32, device=dev)
     lut_ws = torch.empty(65536 * 4, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
+    p2p = strip and world > 1 and args.gather == "p2p"
+    # the C_T buffer the kernels write: local, or (p2p) rank 0's buffer mapped into this rank
+    ct_out = sharding.peer_output(ct if rank == 0 else None, tuple(ct.shape), torch.uint8, rank) if p2p else ct
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
     px_step = B * WT * HT if not strip else B * WT * (re_ - rb)  # pixels this rank outputs
     px_job = world * B * WT * HT if not strip else B * WT * HT
 
@@ -198,17 +206,19 @@ def run_ours(args):
             n = sb.launch_count()
             if record:
                 es[1].record(stream)
-            sb.stylize_batch(prm, cs, gs, lut, gt, frame_seeds=seeds, ct=None if rad > 0 else ct, coords=coords,
+            sb.stylize_batch(prm, cs, gs, lut, gt, frame_seeds=seeds, ct=None if rad > 0 else ct_out, coords=coords,
                              want_level=False)
             n += sb.launch_count()
             if record:
                 es[2].record(stream)
             if rad > 0:
-                sb.vote(coords, cs, rad, ct=ct, row_begin=rb, row_end=re_)
+                sb.vote(coords, cs, rad, ct=ct_out, row_begin=rb, row_end=re_)
                 n += sb.launch_count()
             if record:
                 es[3].record(stream)
-            if strip and world > 1:  # the one exchange step: C_T strips -> rank 0 over NCCL
+            if p2p:  # the strips are already in rank 0's buffer: order rank 0 after every writer
+                dist.all_reduce(flag)
+            elif strip and world > 1:  # the one exchange step: C_T strips -> rank 0 over NCCL
                 sharding.gather_strips(ct[:, rb:re_], HT, world, rank, dst=0, row_axis=1)
             if record:
                 es[4].record(stream)
@@ -369,7 +379,9 @@ def run_ours(args):
                    "frames_per_gpu": B, "global_frames": B * world, "levels": cfg["L"], "threshold": cfg["t"],
                    "blend_radius": r,
                    "parallelism": (f"frame-sharded x{world} (no data-path collective)" if not strip else
-                                   f"row-strip-sharded x{world}, C_T strips gathered to rank 0 (NCCL gather)"),
+                                   f"row-strip-sharded x{world}, C_T strips gathered to rank 0 "
+                                   + ("(kernels store into rank 0's buffer over NVLink peer memory)" if p2p
+                                      else "(NCCL gather)")),
                    "l2": "inputs larger than L2 (G_T %.2f GB per GPU per step); no flush" % (4 * px_step / 1e9)},
         "fps_4k": round(value * 1e6 / (WT * HT), 1),
         "kernels": kernels,

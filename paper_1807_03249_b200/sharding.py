@@ -9,7 +9,11 @@ level and frame seed, so any partition reproduces the single-GPU result bit for 
 * Strip mode (single-frame latency): each frame is cut into row strips, one per rank.  A rank
   computes its strip through sb_params.row_begin/row_end (the vote's r-row coordinate halo is
   recomputed inside the library, so no halo exchange is needed) and the strips are gathered
-  to the consumer rank -- the one real exchange step, done with NCCL over NVLink on GPUs.
+  to the consumer rank -- the one real exchange step.  Two ways: `gather_strips` (one NCCL
+  gather after the compute), or `peer_output` (the consumer's output buffer is mapped into
+  every rank through CUDA IPC and each rank's stylize kernel stores its rows straight into it
+  over NVLink / NVSwitch, so the transfer overlaps the compute tile by tile; a one-element
+  all-reduce then orders the consumer after every writer).
 
 The functions take a torch.distributed process group and work with any backend (NCCL for
 CUDA tensors, gloo for the CPU tests in tests/test_sharding_gloo.py).  Compute is passed in
@@ -61,6 +65,36 @@ def gather_strips(strip: torch.Tensor, ht: int, world: int, rank: int, dst: int 
         return out
     dist.gather(pad, gather_list=None, dst=dst, group=group)
     return None
+
+
+def _share_cuda_ipc(t: torch.Tensor):
+    return t.untyped_storage()._share_cuda_()
+
+
+def _open_cuda_ipc(handle, shape, dtype):
+    storage = torch.UntypedStorage._new_shared_cuda(*handle)
+    out = torch.empty(0, dtype=dtype, device=storage.device)
+    strides, acc = [], 1
+    for n in reversed(shape):
+        strides.insert(0, acc)
+        acc *= n
+    out.set_(storage, 0, tuple(shape), tuple(strides))
+    return out
+
+
+def peer_output(local: torch.Tensor | None, shape, dtype, rank: int, src: int = 0, group=None,
+                share: Callable | None = None, open_: Callable | None = None):
+    """Rank src's output tensor, mapped into every rank: on src `local` itself, elsewhere a
+    tensor over the same device memory (CUDA IPC), whose pointer a kernel on this rank's GPU
+    stores to over NVLink / NVSwitch peer access.  The handle travels with one object
+    broadcast.  `share` / `open_` default to CUDA IPC; tests pass stand-ins."""
+    share = share or _share_cuda_ipc
+    open_ = open_ or _open_cuda_ipc
+    obj = [share(local) if rank == src else None]
+    dist.broadcast_object_list(obj, src=src, group=group)
+    if rank == src:
+        return local
+    return open_(obj[0], shape, dtype)
 
 
 def stylize_strip_mode(compute: Callable[[int, int], torch.Tensor], ht: int, world: int, rank: int, dst: int = 0,

@@ -92,3 +92,51 @@ def test_strip_mode_gather_world2(r):
         assert p.exitcode == 0
     results = [q.get(timeout=10) for _ in range(2 * world)]
     assert all(results), results
+
+
+def _peer_worker(rank, world, port, path, q):
+    """Strip mode with the consumer's buffer mapped into every rank (sharding.peer_output):
+    each rank writes only its own rows straight into rank 0's buffer, a barrier orders rank 0
+    after the writers.  CUDA IPC is replaced by a file mapping (the same host logic)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = synth.CONFIGS[1]
+        cs, gs = [t.numpy() for t in synth.exemplar(cfg)]
+        gt = synth.heightfield_normals(40, 37, seed=2).numpy()
+        lut = oracle.build_lut(gs)
+        prm = oracle.Params(t=cfg["t"], L=3, C=3, seed=cfg["seed"])
+        shape = (37, 40, 4)
+        local = None
+        if rank == 0:
+            local = torch.from_numpy(np.memmap(path, dtype=np.uint8, mode="w+", shape=shape))
+            local.fill_(0)
+        share = lambda t: path  # noqa: E731
+        open_ = lambda h, shp, dt: torch.from_numpy(np.memmap(h, dtype=np.uint8, mode="r+", shape=shp))  # noqa: E731
+        out = sharding.peer_output(local, shape, torch.uint8, rank, share=share, open_=open_)
+        b, e = sharding.strip_rows(shape[0], world, rank)
+        out[b:e] = _strip_compute(prm, cs, gs, lut, gt, 0, b, e)  # the "kernel" stores its rows
+        dist.barrier()  # stands in for the stream-ordered all-reduce after the writers' kernels
+        if rank == 0:
+            _, coords, _ = oracle.stylize(prm, cs, gs, lut, gt)
+            q.put(bool((out.numpy() == cs[coords >> 16, coords & 0xFFFF]).all()))
+        else:
+            q.put(True)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_strip_mode_peer_output_world2(tmp_path):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    path = str(tmp_path / "ct.bin")
+    procs = [ctx.Process(target=_peer_worker, args=(k, world, port, path, q)) for k in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    results = [q.get(timeout=10) for _ in range(world)]
+    assert all(results), results
