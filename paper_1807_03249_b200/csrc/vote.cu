@@ -79,7 +79,7 @@ __device__ __forceinline__ void swar_add(uint32_t c, uint32_t& lo, uint32_t& hi)
 }  // namespace
 
 template <int R>
-__global__ void __launch_bounds__(NT, (R <= 3 ? 8 : 2)) vote_kernel(const VoteArgs a) {
+__global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteArgs a) {
     constexpr int SW = TW + 2 * R, SH = TH + 2 * R;
     constexpr int KR = (R + 3) / 4;           // 16-byte words covering the halo
     constexpr int OFF = 4 * KR;               // tile column x is stored at sc[.][OFF + x]
