@@ -275,11 +275,25 @@ def run_ours(args):
     # measured DRAM traffic of the same kernel: one `ncu --set full` capture (profiles/traffic.json,
     # written by tools/ncu_traffic.py), per pixel, scaled to this launch
     traffic = None
+    roof_issue = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f)
         key = dom if not (dom == "stylize" and r > 0) else "stylize_coords"
         traffic = round(tj[key]["bytes_per_px"] * px_step)
+        # the bound the kernel actually meets: instruction issue.  Peak = SMs x 4
+        # schedulers x 1 warp-instruction/clock at the max SM clock; achieved = the warp
+        # instructions per pixel of the ncu capture x the pixels per second measured here.
+        ipp = tj[key].get("warp_inst_per_px")
+        if ipp:
+            props = torch.cuda.get_device_properties(dev)
+            mhz = main["clocks"].get("sm_max_mhz") or 1965
+            peak_i = props.multi_processor_count * 4 * mhz * 1e6
+            ach_i = ipp * px_step / (kt[dom] * 1e-3)
+            roof_issue = {"bound": "alu", "kernel": dom, "achieved": round(ach_i / 1e9, 1),
+                          "peak": round(peak_i / 1e9, 1), "unit": "G warp-instructions/s",
+                          "frac": round(ach_i / peak_i, 4), "warp_inst_per_px": round(ipp, 3),
+                          "peak_source": "SMs x 4 issue slots x max SM clock (B200_PROFILING.md unit counts)"}
     except Exception:
         pass
     kernels = main["kernels"]
@@ -385,6 +399,7 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (G_T %.2f GB per GPU per step); no flush" % (4 * px_step / 1e9)},
         "fps_4k": round(value * 1e6 / (WT * HT), 1),
         "kernels": kernels,
+        "roofline_issue": roof_issue,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(ach / hbm, 4), "traffic": traffic, "peak_source": hbm_src,
                      "alg_bytes_per_launch": alg[dom], "alg_bytes_per_px": alg[dom] // px_step},

@@ -1,6 +1,7 @@
 """Turn one `ncu --set full` capture of the bench's stylize/vote launches (profiles/gpu_iter.sh:
 main stylize with blit colours, the blend run's coords-only stylize, the vote) into per-pixel DRAM
-traffic (dram__bytes_read.sum + dram__bytes_write.sum per launch / pixels per launch).
+traffic (dram__bytes_read.sum + dram__bytes_write.sum per launch / pixels per launch) and warp
+instructions per pixel (smsp__inst_executed.sum / pixels: the input of bench.py's issue roofline).
 
 usage: python tools/ncu_traffic.py <report.ncu-rep> <frames_per_launch> <out.json>
 bench.py reads profiles/traffic.json and scales it to its own launch size.
@@ -29,7 +30,8 @@ for row in rows[2:]:
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     rd = float(d["dram__bytes_read.sum"]) * scale[unit_r]
     wr = float(d["dram__bytes_write.sum"]) * scale[unit_w]
+    inst = float(d["smsp__inst_executed.sum"])
     res[key] = {"dram_read_bytes": rd, "dram_write_bytes": wr, "pixels": px,
-                "bytes_per_px": (rd + wr) / px, "kernel": name, "report": rep}
+                "bytes_per_px": (rd + wr) / px, "warp_inst_per_px": inst / px, "kernel": name, "report": rep}
 json.dump(res, open(out, "w"), indent=2)
 print(json.dumps(res, indent=2))
