@@ -1,8 +1,8 @@
 // stylize.cu -- tiled Alg. 2 "ParallelStyleBlit" for sm_100a.
 //
 // One CTA = one 128 x 32 pixel tile of one frame (grid = tiles_x x tiles_y x frames), 256
-// threads; warp w owns tile rows w, w+8, w+16, w+24 and a thread owns 4 consecutive pixels of
-// each (uint4 I/O).  Per tile and level l the seed cells that any tile pixel can reach (its
+// threads; warp w owns tile rows 4w .. 4w+3 and a thread owns 4 consecutive pixels of each
+// (uint4 I/O), i.e. a 4 x 4 pixel block.  Per tile and level l the seed cells that any tile pixel can reach (its
 // 3x3 neighbourhood) are materialised in shared memory:
 //     cell = (32*(s.x - x0), 32*(s.y - y0), delta),  delta = u* - q packed as dy*65536 + dx,
 // where s is the jittered seed (SeedPoint, lines 354-358), q = clamp(s) (reading R8) and
@@ -38,7 +38,7 @@ constexpr int NT = 256;           // threads per CTA
 constexpr int TP = TW * TH;       // pixels per tile
 constexpr int NG = TW / 4;        // 4-pixel groups per row
 constexpr int NW = NT / 32;       // warps per CTA
-constexpr int RPW = TH / NW;      // rows per warp (w, w + 8, ...)
+constexpr int RPW = TH / NW;      // rows per warp (RPW w .. RPW w + RPW-1)
 constexpr int WPX = TP / NW;      // pixels per warp
 // tables kept at once: levels {L, L-1, L-2} with h >= 4, i.e. at most levels 4, 3, 2
 // Tables are column-major with a fixed column stride CS = 13 cells (208 bytes = 52 words: 8
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
     const int rows_here = min(TH, a.row_end - y0);
     const int L = a.L;
     // tile row of this warp's j-th row, and whether its group exists
-    auto row_of = [&](int j) { return warp + NW * j; };
+    auto row_of = [&](int j) { return RPW * warp + j; };  // the thread's 4 groups form a 4x4 block
     auto ok_of = [&](int j) { return colok && row_of(j) < rows_here; };
 
     // ---- tables of the levels among L, L-1, L-2 with h >= 4: the only CTA barrier ----
