@@ -6,7 +6,7 @@ writes real-valued formulas).  Only ``tests/``, ``__graft_entry__.smoke()`` and
 The product package ``paper_1807_03249_b200`` never imports it and shares no code with it.
 
 Every function follows PAPER.md Alg. 2 (lines 337-393) and the voting paragraph
-(lines 412-421); the readings of ambiguous passages (R1..R20) are listed in DESIGN.md.
+(lines 412-421); the readings of ambiguous passages (R1..R27) are listed in DESIGN.md.
 Parity of every function is pinned by tests/test_oracle_*.py.
 """
 from __future__ import annotations

@@ -8,7 +8,7 @@
  * Plain C99, fp64 where the paper writes a real-valued formula, written in the paper's
  * order and notation (Alg. 2; voting, lines 412-421).  No
  * blocking, no tables, no reordering: it is meant to be checked against the paper by eye.
- * Readings R1..R20 of ambiguous passages are listed in DESIGN.md.
+ * Readings R1..R27 of ambiguous passages are listed in DESIGN.md.
  *
  * Pins (tests/test_oracle_*.py, -m "not gpu"): SURVEY App. A hash vectors, SPEC's
  * worked SeedPoint/NearestSeed examples, closed-form NearestSeed on the zero-jitter

@@ -9,7 +9,7 @@
  * paper_1807_03249_b200/ (the product), and the product never loads it.
  *
  * Every open point of the paper is fixed by a numbered reading listed in
- * DESIGN.md ("Readings"); the numbers R1..R20 below refer to that list.
+ * DESIGN.md ("Readings"); the numbers R1..R27 below refer to that list.
  *
  * Images: row-major, 4 bytes per pixel (uint8 x4), pixel (x,y) at byte 4*(y*W+x).
  * Coordinates returned packed as x | y<<16 (uint32).
