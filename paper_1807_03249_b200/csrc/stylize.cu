@@ -46,14 +46,26 @@ constexpr int WPX = TP / NW;      // pixels per warp
 // different columns do not conflict).  CS >= TH/4 + 4, the most cells a column of a level
 // with h = 4 spans.
 constexpr int CS = 13;
-constexpr int cells_of(int h) { return (TW / h + 3) * CS; }
+__host__ __device__ constexpr int cells_of(int h) { return (TW / h + 3) * CS; }
 constexpr int MAXCELLS = cells_of(4) + cells_of(8) + cells_of(16);
+// table slots for a hierarchy of L levels: levels L, L-1, L-2 that have h >= 4
+__host__ __device__ constexpr int table_cells(int L) {
+    return (L >= 2 ? cells_of(1 << L) : 0) + (L - 1 >= 2 ? cells_of(1 << (L - 1)) : 0) +
+           (L - 2 >= 2 ? cells_of(1 << (L - 2)) : 0);
+}
 
+// Shared memory: this head, then the cell tables (table_cells(L) slots, column-major per level,
+// slot = off + ci*CS + cj) as two arrays, then the level map when requested:
+//   cq[slot] = (S2, X1)      the NearestSeed key terms (see KOFS below)
+//   cd[slot] = (Y1, delta)   delta = u* - q packed dy*65536 + dx
 struct Smem {
     uint32_t coord[TP];           // result coords
     uint16_t wq[NW][WPX];         // per-warp pixel queue (compacted in place)
     uint16_t glist[NW][RPW * NG]; // per-warp list of groups with a rejected pixel
-    int4 cell[MAXCELLS];          // seed/offset tables, column-major per level (ci*CS + cj)
+};
+struct Cells {
+    uint2* q;
+    int2* d;
 };
 
 struct CellGrid {
@@ -70,7 +82,22 @@ __device__ __forceinline__ CellGrid cell_grid(int x0, int y0, int l, int off) {
     return g;
 }
 
-__device__ __forceinline__ void build_one(Smem& sm, const StylizeArgs& a, const uint32_t* __restrict__ gtf, int x0,
+// NearestSeed keys (Alg. 2).  For a seed s and pixel p of a tile with origin
+// (x0, y0), let S = 32 (s - origin), P = 32 (p - origin) = 32 (rx, ry).  A cell stores
+//     S2 = |S|^2 + idx + KOFS,  X1 = -64 Sx,  Y1 = -64 Sy   (mod 2^32),
+// idx = the cell's slot in the table, so that
+//     key = S2 + rx X1 + ry Y1 = |S - P|^2 - |P|^2 + idx + KOFS = 1024 d + idx + KOFS - |P|^2.
+// |P|^2 is the same for all 9 candidates of p, so the keys order p's candidates by d, then by
+// idx.  The tables are column-major with cj < CS, so idx orders the 3 x 3 candidates like
+// Alg. 2's loops (x outer, y inner): the minimum key is the first strict minimum (reading R7),
+// and its low 10 bits (idx < 1024) address the winner.  Neighbouring pixels differ by one
+// table word: key(rx + i, ry + r) = key(rx, ry) + i X1 + r Y1, one fused add-min (VIADDMNMX)
+// per key.  KOFS = 1024 (132^2 + 32^2) > |P|^2 keeps every key >= 0, and
+// 1024 d + idx + KOFS < 2^32 for d < 8 h^2, h <= 2^9 (tabled levels, see the launcher).
+constexpr uint32_t KOFS = 1024u * (132u * 132u + 32u * 32u);
+static_assert(MAXCELLS <= 1024, "cell index must fit the key's low 10 bits");
+
+__device__ __forceinline__ void build_one(const Cells& T, const StylizeArgs& a, const uint32_t* __restrict__ gtf, int x0,
                                           int y0, int l, uint32_t c_l, const CellGrid& g, int c) {
     // c < ncx*ncy <= 1000: (c + 0.5) / ncy is >= 0.007 away from an integer, float-exact floor
     const int ci = (int)(((float)c + 0.5f) * __frcp_rn((float)g.ncy));
@@ -82,16 +109,14 @@ __device__ __forceinline__ void build_one(Smem& sm, const StylizeArgs& a, const 
     const uint32_t u = __ldg(a.lut + (__ldg(gtf + (uint32_t)(qy * a.wt + qx)) & a.key_mask));
     // delta = u* - q packed as dy*65536 + dx: p_packed + delta is the packed candidate s
     const int dpack = ((int)(u >> 16) - qy) * 65536 + ((int)(u & 0xFFFFu) - qx);
-    sm.cell[g.off + ci * CS + cj] = make_int4(32 * (sx - x0), 32 * (sy - y0), dpack, 0);
+    const int idx = g.off + ci * CS + cj;
+    const uint32_t Sx = (uint32_t)(32 * (sx - x0)), Sy = (uint32_t)(32 * (sy - y0));
+    const uint32_t S2 = Sx * Sx + Sy * Sy + (uint32_t)idx + KOFS;
+    const uint32_t X1 = 0u - 64u * Sx;
+    T.q[idx] = make_uint2(S2, X1);
+    T.d[idx] = make_int2((int)(0u - 64u * Sy), dpack);
 }
 
-// NearestSeed key of a candidate: 1024 |s - p|^2 + code, code = 16 ((x+1) CS + (y+1)) = the
-// candidate's byte offset in the table relative to cell (-1,-1) of p.  Ordered by d, then by
-// Alg. 2's loop order (x outer, y inner): the minimum is the first strict minimum (reading R7),
-// and its low 10 bits address the winner's cell directly.  1024 d + code < 2^32 needs
-// d < 8 h^2 <= 2^22, i.e. h <= 2^9 for a tabled level (launcher: L <= 9 + ... see below).
-constexpr uint32_t code_of(int x, int y) { return 16u * (uint32_t)((x + 1) * CS + (y + 1)); }
-constexpr int CODE0 = 16 * (CS + 1);  // byte offset of cell (0,0) relative to cell (-1,-1)
 
 __device__ __forceinline__ uint32_t min3u(uint32_t a, uint32_t b, uint32_t c) { return min(min(a, b), c); }
 
@@ -136,83 +161,80 @@ __device__ __forceinline__ bool accept(const StylizeArgs& a, const uint32_t* __r
     return inb & (guide_d2(gp, g, a.cmask) < a.T2);
 }
 
-// NearestSeed (Alg. 2) for the 4 pixels (px0..px0+3, py) of a group, h >= 4:
-// they share their home cell, so the 9 seed loads and the dy terms are shared, and with
-// dx = 32 (s.x - px0), key_i = 1024 ((s.x - px0 - i)^2 + dy^2) + code = A - 64 i dx + 1024 i^2.
-// Returns the table address of cell (-1,-1) of the home cell; the winner of pixel i is the
-// cell at byte offset key[i] & 1023 from it.
-__device__ __forceinline__ const unsigned char* group_ns(const Smem& sm, const CellGrid& g, int l, int x0, int y0,
-                                                        int rx0, int ry, uint32_t key[4]) {
-    const int py = y0 + ry, px0 = x0 + rx0;
-    const int4* cb = &sm.cell[g.off + ((px0 >> l) - g.cx0 - 1) * CS + ((py >> l) - g.cy0 - 1)];
-    uint32_t k0 = 0xFFFFFFFFu, k1 = k0, k2 = k0, k3 = k0;
-    const int R32x = 32 * rx0, R32y = 32 * ry;
+// Slot of the home cell's (-1,-1) neighbour in a level table (column-major, stride CS).
+__device__ __forceinline__ int home_slot(const CellGrid& g, int l, int px, int py) {
+    return g.off + ((px >> l) - g.cx0 - 1) * CS + ((py >> l) - g.cy0 - 1);
+}
+
+// NearestSeed for the 4 pixels (x0+rx0+i, y0+ry) of a group, h >= 4: they share their home
+// cell; per candidate A = key of pixel 0 (2 IMAD) and key_i = A + X_i (fused add-min).
+__device__ __forceinline__ void group_ns(const Cells& T, const CellGrid& g, int l, int x0, int y0, int rx0, int ry,
+                                         uint32_t key[4]) {
+    const int h0 = home_slot(g, l, x0 + rx0, y0 + ry);
 #pragma unroll
-    for (int x = -1; x <= 1; ++x) {
+    for (int c = 0; c < 9; ++c) {
+        const int slot = h0 + (c / 3) * CS + (c % 3);  // x = c/3 - 1 outer, y = c%3 - 1 inner
+        const uint2 s = T.q[slot];
+        const uint32_t Y1 = (uint32_t)T.d[slot].x;
+        const uint32_t A = s.x + (uint32_t)rx0 * s.y + (uint32_t)ry * Y1;
+        const uint32_t X2 = s.y + s.y, X3 = X2 + s.y;
+        const uint32_t kc[4] = {A, A + s.y, A + X2, A + X3};
 #pragma unroll
-        for (int y = -1; y <= 1; ++y) {
-            const int2 s = *reinterpret_cast<const int2*>(&cb[(x + 1) * CS + (y + 1)]);
-            const int dy = s.y - R32y;
-            const int dx = s.x - R32x;
-            const uint32_t A = (uint32_t)(dx * dx) + (uint32_t)(dy * dy) + code_of(x, y);
-            k0 = min(k0, A);
-            k1 = min(k1, A - 64u * (uint32_t)dx + 1024u);
-            k2 = min(k2, A - 128u * (uint32_t)dx + 4096u);
-            k3 = min(k3, A - 192u * (uint32_t)dx + 9216u);
+        for (int i = 0; i < 4; ++i) key[i] = c == 0 ? kc[i] : min(key[i], kc[i]);
+    }
+}
+
+// NearestSeed for the thread's whole 4 x 4 block (pixels x0+rx0+i, y0+ry0+r; 4-aligned, h >= 4):
+// the 16 pixels share their home cell, so per candidate the seed load, A = key of pixel (0,0)
+// and the row bases B_r = A + r Y1 are computed once, and each of the 16 keys costs one fused
+// add-min.
+__device__ __forceinline__ void block_ns(const Cells& T, const CellGrid& g, int l, int x0, int y0, int rx0, int ry0,
+                                         uint32_t key[4][4]) {
+    const int h0 = home_slot(g, l, x0 + rx0, y0 + ry0);
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+        const int slot = h0 + (c / 3) * CS + (c % 3);
+        const uint2 s = T.q[slot];
+        const uint32_t Y1 = (uint32_t)T.d[slot].x;
+        uint32_t B = s.x + (uint32_t)rx0 * s.y + (uint32_t)ry0 * Y1;
+        const uint32_t X2 = s.y + s.y, X3 = X2 + s.y;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (r > 0) B += Y1;
+            const uint32_t kc[4] = {B, B + s.y, B + X2, B + X3};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) key[r][i] = c == 0 ? kc[i] : min(key[r][i], kc[i]);
         }
     }
-    key[0] = k0;
-    key[1] = k1;
-    key[2] = k2;
-    key[3] = k3;
-    return reinterpret_cast<const unsigned char*>(cb);
 }
 
-// delta = u* - q of the winning cell (the .z word of the table entry)
-__device__ __forceinline__ uint32_t winner_delta(const unsigned char* cb, uint32_t key) {
-    return (uint32_t)reinterpret_cast<const int4*>(cb + (key & 1023u))->z;
+// delta = u* - q of the winning cell
+__device__ __forceinline__ uint32_t winner_delta(const Cells& T, uint32_t key) {
+    return (uint32_t)T.d[key & 1023u].y;
 }
 
-// Alg. 2 at level l (h >= 4) for the 4 pixels (px0..px0+3, py) that share one cell: the 9
-// seed loads and dy terms are shared, key_i = 16*((dx - i)^2 + dy^2) + idx = A - 8 i dx4 +
-// 16 i^2.  Writes the 4 packed candidates; returns the acceptance bits.
+// Alg. 2 at level l (h >= 4) for the 4 pixels (px0..px0+3, py) that share one cell.  Writes the
+// 4 packed candidates; returns the acceptance bits.
 template <bool EXT>
-__device__ __forceinline__ uint32_t group_eval(const Smem& sm, const StylizeArgs& a, const uint32_t* __restrict__ gs,
+__device__ __forceinline__ uint32_t group_eval(const Cells& T, const StylizeArgs& a, const uint32_t* __restrict__ gs,
                                                const CellGrid& g, int l, int x0, int y0, int rx0, int ry, uint4 gp4,
-                                               uint32_t cand[4]) {
+                                               uint32_t m, uint32_t cand[4]) {
     uint32_t keys[4];
-    const unsigned char* cb = group_ns(sm, g, l, x0, y0, rx0, ry, keys);
+    group_ns(T, g, l, x0, y0, rx0, ry, keys);
     const uint32_t gpv[4] = {gp4.x, gp4.y, gp4.z, gp4.w};
     const uint32_t p0 = ((uint32_t)(y0 + ry) << 16) | (uint32_t)(x0 + rx0);
     uint32_t acc = 0;
+    // only the pixels in m (still rejected) look up their winner and gather: the others issue
+    // no shared or global request
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const uint32_t c = p0 + (uint32_t)i + winner_delta(cb, keys[i]);
-        cand[i] = c;
-        acc |= (uint32_t)accept<EXT>(a, gs, gpv[i], c) << i;
+        {
+            const uint32_t c = p0 + (uint32_t)i + winner_delta(T, keys[i]);
+            cand[i] = c;
+            acc |= (uint32_t)accept<EXT>(a, gs, gpv[i], c) << i;
+        }
     }
     return acc;
-}
-
-// group_eval split in two for software pipelining: group_issue does NearestSeed, forms the 4
-// candidates and issues their G_S gathers; group_test (called later, after other work has
-// covered the gather latency) applies the threshold.
-__device__ __forceinline__ uint32_t group_issue(const Smem& sm, const StylizeArgs& a, const uint32_t* __restrict__ gs,
-                                                const CellGrid& g, int l, int x0, int y0, int rx0, int ry,
-                                                uint32_t cand[4], uint32_t gv[4]) {
-    uint32_t keys[4];
-    const unsigned char* cb = group_ns(sm, g, l, x0, y0, rx0, ry, keys);
-    const uint32_t p0 = ((uint32_t)(y0 + ry) << 16) | (uint32_t)(x0 + rx0);
-    uint32_t inb = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const uint32_t c = p0 + (uint32_t)i + winner_delta(cb, keys[i]);
-        cand[i] = c;
-        bool in;
-        gv[i] = gather_gs(a, gs, c, &in);
-        inb |= (uint32_t)in << i;
-    }
-    return inb;
 }
 
 template <bool EXT>
@@ -229,25 +251,23 @@ __device__ __forceinline__ uint32_t group_test(const StylizeArgs& a, uint4 gp4, 
 }
 
 // Alg. 2 at level l for one pixel from the level's shared-memory table.
-__device__ __forceinline__ uint32_t table_candidate(const Smem& sm, const CellGrid& g, int l, int x0, int y0, int rx,
+__device__ __forceinline__ uint32_t table_candidate(const Cells& T, const CellGrid& g, int l, int x0, int y0, int rx,
                                                     int ry) {
     const int px = x0 + rx, py = y0 + ry;
-    const int4* cb = &sm.cell[g.off + ((px >> l) - g.cx0 - 1) * CS + ((py >> l) - g.cy0 - 1)];
-    const int R32x = 32 * rx, R32y = 32 * ry;
+    const int h0 = home_slot(g, l, px, py);
     uint32_t kk[3];
 #pragma unroll
-    for (int x = -1; x <= 1; ++x) {
+    for (int x = 0; x < 3; ++x) {
         uint32_t kx[3];
 #pragma unroll
-        for (int y = -1; y <= 1; ++y) {
-            const int2 s = *reinterpret_cast<const int2*>(&cb[(x + 1) * CS + (y + 1)]);
-            const int dx = s.x - R32x, dy = s.y - R32y;
-            kx[y + 1] = (uint32_t)(dx * dx) + (uint32_t)(dy * dy) + code_of(x, y);
+        for (int y = 0; y < 3; ++y) {
+            const int slot = h0 + x * CS + y;
+            kx[y] = T.q[slot].x + (uint32_t)rx * T.q[slot].y + (uint32_t)ry * (uint32_t)T.d[slot].x;
         }
-        kk[x + 1] = min3u(kx[0], kx[1], kx[2]);
+        kk[x] = min3u(kx[0], kx[1], kx[2]);
     }
     const uint32_t key = min3u(kk[0], kk[1], kk[2]);
-    return (((uint32_t)py << 16) | (uint32_t)px) + winner_delta(reinterpret_cast<const unsigned char*>(cb), key);
+    return (((uint32_t)py << 16) | (uint32_t)px) + winner_delta(T, key);
 }
 
 // Alg. 2 at level l for one pixel, NearestSeed straight from the hash.
@@ -280,10 +300,16 @@ template <bool EXT, bool LVL>
 __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_constant__ StylizeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    uint8_t* lvl = smem_raw + sizeof(Smem);  // result levels (only when a.level != nullptr)
+    const int ncells = table_cells(a.L);
+    Cells T;
+    T.q = reinterpret_cast<uint2*>(smem_raw + sizeof(Smem));
+    T.d = reinterpret_cast<int2*>(T.q + ncells);
+    uint8_t* lvl = reinterpret_cast<uint8_t*>(T.d + ncells);  // result levels (only when a.level != nullptr)
 
     const int x0 = blockIdx.x * TW;
-    const int y0 = a.row_begin + blockIdx.y * TH;
+    // tiles start at row_begin rounded down to a multiple of 4, so a thread's 4 rows are one
+    // 4-aligned block (block_ns); rows before row_begin are computed but never written
+    const int y0 = (a.row_begin & ~3) + blockIdx.y * TH;
     const int frame = blockIdx.z;
     const int64_t fpx = (int64_t)a.wt * a.ht;
     const uint32_t* __restrict__ gtf = reinterpret_cast<const uint32_t*>(a.gt) + fpx * frame;
@@ -296,10 +322,11 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
     const int rx0 = lane * 4;               // this thread's 4-pixel group column
     const bool colok = x0 + rx0 < a.wt;     // wt % 4 == 0: a group is all in or all out
     const int rows_here = min(TH, a.row_end - y0);
+    const int row_lo = a.row_begin - y0;  // > 0 only in the first tile row of an unaligned range
     const int L = a.L;
     // tile row of this warp's j-th row, and whether its group exists
     auto row_of = [&](int j) { return RPW * warp + j; };  // the thread's 4 groups form a 4x4 block
-    auto ok_of = [&](int j) { return colok && row_of(j) < rows_here; };
+    auto ok_of = [&](int j) { return colok && row_of(j) < rows_here && row_of(j) >= row_lo; };
 
     // ---- tables of the levels among L, L-1, L-2 with h >= 4: the only CTA barrier ----
     const bool t0 = L >= 2, t1 = L - 1 >= 2, t2 = L - 2 >= 2;
@@ -314,7 +341,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
         const bool s0 = c < ncL, s1 = c < ncL + ncL1;
         const CellGrid& g = s0 ? gL : (s1 ? gL1 : gL2);
         const int l = s0 ? L : (s1 ? L - 1 : L - 2);
-        build_one(sm, a, gtf, x0, y0, l, level_salt(seed, l), g, c - (s0 ? 0 : (s1 ? ncL : ncL + ncL1)));
+        build_one(T, a, gtf, x0, y0, l, level_salt(seed, l), g, c - (s0 ? 0 : (s1 ? ncL : ncL + ncL1)));
     }
     __syncthreads();
     // From here on a warp only touches its own rows: no further CTA barrier.
@@ -329,22 +356,32 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
         // before row j-1's threshold test, so the G_T load and the G_S gathers of a row are
         // in flight while the next row's NearestSeed runs.
         uint32_t rej = 0;  // 4 bits per row j
+        // the block's G_T rows (the HBM stream) are issued before NearestSeed covers their latency
+        uint4 gp[RPW];
+#pragma unroll
+        for (int j = 0; j < RPW; ++j)
+            gp[j] = ok_of(j) ? *reinterpret_cast<const uint4*>(gtf + (uint32_t)((y0 + row_of(j)) * a.wt + x0 + rx0))
+                             : make_uint4(0u, 0u, 0u, 0u);
+        uint32_t key[RPW][4];
+        block_ns(T, gL, L, x0, y0, rx0, row_of(0), key);
+        // rows pipelined: row j's candidates and G_S gathers are issued before row j-1's test
         uint32_t pcand[4] = {0u, 0u, 0u, 0u}, pgv[4] = {0u, 0u, 0u, 0u}, pinb = 0;
-        uint4 pgp = make_uint4(0u, 0u, 0u, 0u);
-        bool pok = false;
 #pragma unroll
         for (int j = 0; j <= RPW; ++j) {
             uint32_t cand[4], gv[4], inb = 0;
-            uint4 gp4;
-            const bool ok = j < RPW && ok_of(j);
-            if (ok) {
-                const int ry = row_of(j);
-                gp4 = *reinterpret_cast<const uint4*>(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + rx0));
-                inb = group_issue(sm, a, gs, gL, L, x0, y0, rx0, ry, cand, gv);
+            if (j < RPW && ok_of(j)) {
+                const uint32_t p0 = ((uint32_t)(y0 + row_of(j)) << 16) | (uint32_t)(x0 + rx0);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    cand[i] = p0 + (uint32_t)i + winner_delta(T, key[j][i]);
+                    bool in;
+                    gv[i] = gather_gs(a, gs, cand[i], &in);
+                    inb |= (uint32_t)in << i;
+                }
             }
-            if (pok) {
+            if (j >= 1 && ok_of(j - 1)) {
                 const int ry = row_of(j - 1);
-                const uint32_t acc = group_test<EXT>(a, pgp, pgv, pinb);
+                const uint32_t acc = group_test<EXT>(a, gp[j - 1], pgv, pinb);
                 *reinterpret_cast<uint4*>(&sm.coord[ry * TW + rx0]) = make_uint4(pcand[0], pcand[1], pcand[2], pcand[3]);
                 if (LVL) *reinterpret_cast<uint32_t*>(&lvl[ry * TW + rx0]) = 0x01010101u * (uint32_t)L;
                 rej |= (~acc & 0xFu) << (4 * (j - 1));
@@ -356,8 +393,6 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                     pgv[i] = gv[i];
                 }
                 pinb = inb;
-                pgp = gp4;
-                pok = ok;
             }
         }
         // ---- the warp's groups that still have a rejected pixel: lane | j<<5 | mask<<8
@@ -387,7 +422,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                     const int pbase = ry * TW + grx0;
                     const uint4 gp4 = *reinterpret_cast<const uint4*>(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + grx0));
                     uint32_t cand[4];
-                    const uint32_t acc = group_eval<EXT>(sm, a, gs, g, lp, x0, y0, grx0, ry, gp4, cand);
+                    const uint32_t acc = group_eval<EXT>(T, a, gs, g, lp, x0, y0, grx0, ry, gp4, m, cand);
                     // merge the newly accepted pixels into the group's coords: one 16-byte
                     // read-modify-write instead of four conflicting scalar stores
                     const uint32_t take = m & acc;
@@ -465,7 +500,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
             if (k < n) {
                 idx = q[k];
                 const int rx = idx & (TW - 1), ry = idx / TW;
-                const uint32_t cand = table ? table_candidate(sm, g, l, x0, y0, rx, ry)
+                const uint32_t cand = table ? table_candidate(T, g, l, x0, y0, rx, ry)
                                             : direct_candidate(a, gtf, x0 + rx, y0 + ry, l, c_l);
                 const uint32_t gp = __ldg(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + rx));
                 if (accept<EXT>(a, gs, gp, cand)) {
@@ -518,9 +553,8 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
 }
 
 cudaError_t launch_stylize_tiled(const StylizeArgs& a, int n_frames, cudaStream_t st, int* launches) {
-    static_assert(sizeof(Smem) + TP <= 48 * 1024, "smem");
-    // the level map only when requested: without it 4 CTAs leave ~92 KB of L1 per SM
-    const size_t smem = sizeof(Smem) + (a.level ? TP : 0);
+    // tables sized for this L; the level map only when requested
+    const size_t smem = sizeof(Smem) + (size_t)table_cells(a.L) * (sizeof(uint2) + sizeof(int2)) + (a.level ? TP : 0);
     auto kern = a.ext ? (a.level ? stylize_tiled_kernel<true, true> : stylize_tiled_kernel<true, false>)
                       : (a.level ? stylize_tiled_kernel<false, true> : stylize_tiled_kernel<false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -530,7 +564,7 @@ cudaError_t launch_stylize_tiled(const StylizeArgs& a, int n_frames, cudaStream_
         return ev ? atoi(ev) : -1;
     }();
     if (carve >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-    dim3 grid((unsigned)((a.wt + TW - 1) / TW), (unsigned)((a.row_end - a.row_begin + TH - 1) / TH),
+    dim3 grid((unsigned)((a.wt + TW - 1) / TW), (unsigned)((a.row_end - (a.row_begin & ~3) + TH - 1) / TH),
               (unsigned)n_frames);
     kern<<<grid, NT, smem, st>>>(a);
     *launches += 1;
