@@ -99,8 +99,12 @@ static_assert(MAXCELLS <= 1024, "cell index must fit the key's low 10 bits");
 
 __device__ __forceinline__ void build_one(const Cells& T, const StylizeArgs& a, const uint32_t* __restrict__ gtf, int x0,
                                           int y0, int l, uint32_t c_l, const CellGrid& g, int c) {
-    // c < ncx*ncy <= 1000: (c + 0.5) / ncy is >= 0.007 away from an integer, float-exact floor
-    const int ci = (int)(((float)c + 0.5f) * __frcp_rn((float)g.ncy));
+    // c < ncx*ncy <= 1000, ncy <= 13: (c + 0.5) / ncy is >= 0.5/13 away from an integer, so the
+    // floor is exact even with the approximate reciprocal (relative error ~2^-23; the IEEE
+    // __frcp_rn carries a slow-path branch)
+    float rcp;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rcp) : "f"((float)g.ncy));
+    const int ci = (int)(((float)c + 0.5f) * rcp);
     const int cj = c - ci * g.ncy;
     int sx, sy;
     cell_seed(g.cx0 + ci, g.cy0 + cj, l, c_l, a.zero_jitter != 0, sx, sy);
