@@ -300,11 +300,14 @@ __device__ __forceinline__ uint32_t direct_candidate(const StylizeArgs& a, const
 
 }  // namespace
 
-template <bool EXT, bool LVL>
+// LT > 0: the hierarchy depth as a compile-time constant (the common depths; all level geometry
+// folds), LT = 0: a.L at run time.
+template <bool EXT, bool LVL, int LT>
 __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_constant__ StylizeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    const int ncells = table_cells(a.L);
+    const int L = LT > 0 ? LT : a.L;
+    const int ncells = table_cells(L);
     Cells T;
     T.q = reinterpret_cast<uint2*>(smem_raw + sizeof(Smem));
     T.d = reinterpret_cast<int2*>(T.q + ncells);
@@ -327,7 +330,6 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
     const bool colok = x0 + rx0 < a.wt;     // wt % 4 == 0: a group is all in or all out
     const int rows_here = min(TH, a.row_end - y0);
     const int row_lo = a.row_begin - y0;  // > 0 only in the first tile row of an unaligned range
-    const int L = a.L;
     // tile row of this warp's j-th row, and whether its group exists
     auto row_of = [&](int j) { return RPW * warp + j; };  // the thread's 4 groups form a 4x4 block
     auto ok_of = [&](int j) { return colok && row_of(j) < rows_here && row_of(j) >= row_lo; };
@@ -559,8 +561,16 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
 cudaError_t launch_stylize_tiled(const StylizeArgs& a, int n_frames, cudaStream_t st, int* launches) {
     // tables sized for this L; the level map only when requested
     const size_t smem = sizeof(Smem) + (size_t)table_cells(a.L) * (sizeof(uint2) + sizeof(int2)) + (a.level ? TP : 0);
-    auto kern = a.ext ? (a.level ? stylize_tiled_kernel<true, true> : stylize_tiled_kernel<true, false>)
-                      : (a.level ? stylize_tiled_kernel<false, true> : stylize_tiled_kernel<false, false>);
+    void (*kern)(StylizeArgs);
+    if (a.ext) {
+        kern = a.level ? stylize_tiled_kernel<true, true, 0> : stylize_tiled_kernel<true, false, 0>;
+    } else if (a.level) {
+        kern = a.L == 5 ? stylize_tiled_kernel<false, true, 5> : a.L == 4 ? stylize_tiled_kernel<false, true, 4>
+             : a.L == 3 ? stylize_tiled_kernel<false, true, 3> : stylize_tiled_kernel<false, true, 0>;
+    } else {
+        kern = a.L == 5 ? stylize_tiled_kernel<false, false, 5> : a.L == 4 ? stylize_tiled_kernel<false, false, 4>
+             : a.L == 3 ? stylize_tiled_kernel<false, false, 3> : stylize_tiled_kernel<false, false, 0>;
+    }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     static const int carve = [] {
