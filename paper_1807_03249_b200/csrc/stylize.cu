@@ -334,6 +334,14 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
     auto row_of = [&](int j) { return RPW * warp + j; };  // the thread's 4 groups form a 4x4 block
     auto ok_of = [&](int j) { return colok && row_of(j) < rows_here && row_of(j) >= row_lo; };
 
+    // The thread's 4 G_T rows (the HBM stream, consumed at level L) are issued first: their
+    // latency overlaps the table build and its barrier.
+    uint4 gp[RPW];
+#pragma unroll
+    for (int j = 0; j < RPW; ++j)
+        gp[j] = (L >= 2 && ok_of(j)) ? *reinterpret_cast<const uint4*>(gtf + (uint32_t)((y0 + row_of(j)) * a.wt + x0 + rx0))
+                                     : make_uint4(0u, 0u, 0u, 0u);
+
     // ---- tables of the levels among L, L-1, L-2 with h >= 4: the only CTA barrier ----
     const bool t0 = L >= 2, t1 = L - 1 >= 2, t2 = L - 2 >= 2;
     const CellGrid gL = cell_grid(x0, y0, L, 0);
@@ -363,11 +371,6 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
         // in flight while the next row's NearestSeed runs.
         uint32_t rej = 0;  // 4 bits per row j
         // the block's G_T rows (the HBM stream) are issued before NearestSeed covers their latency
-        uint4 gp[RPW];
-#pragma unroll
-        for (int j = 0; j < RPW; ++j)
-            gp[j] = ok_of(j) ? *reinterpret_cast<const uint4*>(gtf + (uint32_t)((y0 + row_of(j)) * a.wt + x0 + rx0))
-                             : make_uint4(0u, 0u, 0u, 0u);
         uint32_t key[RPW][4];
         block_ns(T, gL, L, x0, y0, rx0, row_of(0), key);
         // rows pipelined: row j's candidates and G_S gathers are issued before row j-1's test
