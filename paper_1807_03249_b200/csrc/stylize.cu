@@ -391,7 +391,12 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
             if (j >= 1 && ok_of(j - 1)) {
                 const int ry = row_of(j - 1);
                 const uint32_t acc = group_test<EXT>(a, gp[j - 1], pgv, pinb);
-                *reinterpret_cast<uint4*>(&sm.coord[ry * TW + rx0]) = make_uint4(pcand[0], pcand[1], pcand[2], pcand[3]);
+                // a rejected pixel's slot holds its G_T value until a finer level accepts it
+                // (the group passes and the pixel queue read it from there, not from global)
+                const uint4 g4 = gp[j - 1];
+                *reinterpret_cast<uint4*>(&sm.coord[ry * TW + rx0]) =
+                    make_uint4((acc & 1u) ? pcand[0] : g4.x, (acc & 2u) ? pcand[1] : g4.y,
+                               (acc & 4u) ? pcand[2] : g4.z, (acc & 8u) ? pcand[3] : g4.w);
                 if (LVL) *reinterpret_cast<uint32_t*>(&lvl[ry * TW + rx0]) = 0x01010101u * (uint32_t)L;
                 rej |= (~acc & 0xFu) << (4 * (j - 1));
             }
@@ -429,13 +434,13 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                     const int ry = row_of((int)((e >> 5) & 7u));
                     const uint32_t m = e >> 8;
                     const int pbase = ry * TW + grx0;
-                    const uint4 gp4 = *reinterpret_cast<const uint4*>(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + grx0));
-                    uint32_t cand[4];
-                    const uint32_t acc = group_eval<EXT>(T, a, gs, g, lp, x0, y0, grx0, ry, gp4, m, cand);
-                    // merge the newly accepted pixels into the group's coords: one 16-byte
-                    // read-modify-write instead of four conflicting scalar stores
-                    const uint32_t take = m & acc;
+                    // the group's slots: coords of its accepted pixels, G_T of the rejected (m)
                     uint4 cv = *reinterpret_cast<const uint4*>(&sm.coord[pbase]);
+                    uint32_t cand[4];
+                    const uint32_t acc = group_eval<EXT>(T, a, gs, g, lp, x0, y0, grx0, ry, cv, m, cand);
+                    // merge the newly accepted pixels: one 16-byte read-modify-write instead of
+                    // four conflicting scalar stores
+                    const uint32_t take = m & acc;
                     cv.x = (take & 1u) ? cand[0] : cv.x;
                     cv.y = (take & 2u) ? cand[1] : cv.y;
                     cv.z = (take & 4u) ? cand[2] : cv.z;
@@ -490,6 +495,9 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
         for (int j = 0; j < RPW; ++j) {
             if (!ok_of(j)) continue;
             for (int i = 0; i < 4; ++i) q[pos++] = (uint16_t)(row_of(j) * TW + rx0 + i);
+            // the queue reads G_T from the pixel's slot
+            *reinterpret_cast<uint4*>(&sm.coord[row_of(j) * TW + rx0]) =
+                *reinterpret_cast<const uint4*>(gtf + (uint32_t)((y0 + row_of(j)) * a.wt + x0 + rx0));
         }
         n = tot;
         l = 1;
@@ -511,7 +519,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                 const int rx = idx & (TW - 1), ry = idx / TW;
                 const uint32_t cand = table ? table_candidate(T, g, l, x0, y0, rx, ry)
                                             : direct_candidate(a, gtf, x0 + rx, y0 + ry, l, c_l);
-                const uint32_t gp = __ldg(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + rx));
+                const uint32_t gp = sm.coord[idx];  // G_T while the pixel is rejected
                 if (accept<EXT>(a, gs, gp, cand)) {
                     sm.coord[idx] = cand;
                     if (LVL) lvl[idx] = (uint8_t)l;
@@ -532,8 +540,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
         for (int k = lane; k < n; k += 32) {
             const int idx = q[k];
             const int rx = idx & (TW - 1), ry = idx / TW;
-            const uint32_t gp = __ldg(gtf + (uint32_t)((y0 + ry) * a.wt + x0 + rx));
-            sm.coord[idx] = __ldg(a.lut + (gp & a.key_mask));
+            sm.coord[idx] = __ldg(a.lut + (sm.coord[idx] & a.key_mask));  // the slot holds G_T
             if (LVL) lvl[idx] = 0;
         }
     }
