@@ -2,28 +2,29 @@
 //
 // One CTA = one 128 x 32 pixel tile of one frame (grid = tiles_x x tiles_y x frames), 256
 // threads; warp w owns tile rows 4w .. 4w+3 and a thread owns 4 consecutive pixels of each
-// (uint4 I/O), i.e. a 4 x 4 pixel block.  Per tile and level l the seed cells that any tile pixel can reach (its
-// 3x3 neighbourhood) are materialised in shared memory:
-//     cell = (32*(s.x - x0), 32*(s.y - y0), delta),  delta = u* - q packed as dy*65536 + dx,
-// where s is the jittered seed (SeedPoint, lines 354-358), q = clamp(s) (reading R8) and
-// u* = LUT[G_T[q]] (line 383).  A pixel's candidate is then s = p + delta of its nearest seed
-// (line 384), so per pixel and level the work is 9 shared-memory distance evaluations, one
-// L2-resident gather of G_S[s] and a 3-instruction squared error (VABSDIFF4+LOP3+IDP.4A).
+// (uint4 I/O), i.e. a 4-aligned 4 x 4 pixel block.  Per tile and level l the seed cells that
+// any tile pixel can reach (its 3x3 neighbourhood) are materialised in
+// shared memory: the NearestSeed key words of the jittered seed s (SeedPoint, lines 354-358;
+// see KOFS) and delta = u* - q, q = clamp(s) (reading R8), u* = LUT[G_T[q]] (line 383).  A
+// pixel's candidate is s = p + delta of its nearest seed (line 384), so per pixel and level the
+// work is 9 shared-memory key evaluations, one L2-resident gather of G_S[s] and a
+// 3-instruction squared error (VABSDIFF4+LOP3+IDP.4A).
 //
 // Levels run coarse to fine with compaction:
-//   level L    every 4-pixel group (the pixels of a 4-aligned group share their cell for
-//              h >= 4, so the 9 seed loads and the dy terms are shared by 4 pixels),
-//              software-pipelined over the thread's 4 rows;
-//   L-1, L-2   only the groups with a rejected pixel, densely from a warp-local group list
-//              compacted in place, same shared-cell evaluation;
-//   below      the remaining pixels from a warp-local pixel queue, one per lane.
+//   level L    the thread's whole 4 x 4 block at once (its 16 pixels share their home cell for
+//              h >= 4: one table load per candidate, one add + one min per key), rows
+//              software-pipelined;
+//   L-1, L-2   only the 4-pixel groups with a rejected pixel, densely from a warp-local group
+//              list compacted in place, same shared-cell evaluation per group;
+//   below      the remaining pixels from a warp-local pixel queue, one per lane, NearestSeed
+//              from the hash (h = 2 and finer have no table).
 // The tables of the levels L, L-1, L-2 that have h >= 4 are built together up front, behind
 // the kernel's only CTA barrier; afterwards each warp works on its own rows with warp-local
-// lists (ballot/scan compaction, __syncwarp only), so warps never wait for each other.  Levels
-// without a table (h = 2, or below L-2) evaluate their 9 seeds straight from the hash.  Pixels
-// left after level 1 take the level-0 look-up (reading R12).
+// lists (ballot/scan compaction, __syncwarp only), so warps never wait for each other.  Pixels
+// left after level 1 take the level-0 look-up (reading R12).  A rejected pixel's coords slot
+// holds its G_T value until a finer level accepts it.
 //
-// NearestSeed ties: see code_of() -- the key 1024 d + code orders by d, then by Alg. 2's loop
+// NearestSeed ties: see KOFS -- the key 1024 d + slot orders by d, then by Alg. 2's loop
 // order (x outer, y inner), so the minimum key is the first strict minimum (reading R7).
 #include <cstdlib>
 
@@ -122,7 +123,6 @@ __device__ __forceinline__ void build_one(const Cells& T, const StylizeArgs& a, 
 }
 
 
-__device__ __forceinline__ uint32_t min3u(uint32_t a, uint32_t b, uint32_t c) { return min(min(a, b), c); }
 
 // Exclusive warp prefix sum of v; *total receives the warp-wide sum.
 __device__ __forceinline__ int warp_excl_scan(int v, int* total) {
@@ -252,26 +252,6 @@ __device__ __forceinline__ uint32_t group_test(const StylizeArgs& a, uint4 gp4, 
         acc |= (uint32_t)ok << i;
     }
     return acc & inb;
-}
-
-// Alg. 2 at level l for one pixel from the level's shared-memory table.
-__device__ __forceinline__ uint32_t table_candidate(const Cells& T, const CellGrid& g, int l, int x0, int y0, int rx,
-                                                    int ry) {
-    const int px = x0 + rx, py = y0 + ry;
-    const int h0 = home_slot(g, l, px, py);
-    uint32_t kk[3];
-#pragma unroll
-    for (int x = 0; x < 3; ++x) {
-        uint32_t kx[3];
-#pragma unroll
-        for (int y = 0; y < 3; ++y) {
-            const int slot = h0 + x * CS + y;
-            kx[y] = T.q[slot].x + (uint32_t)rx * T.q[slot].y + (uint32_t)ry * (uint32_t)T.d[slot].x;
-        }
-        kk[x] = min3u(kx[0], kx[1], kx[2]);
-    }
-    const uint32_t key = min3u(kk[0], kk[1], kk[2]);
-    return (((uint32_t)py << 16) | (uint32_t)px) + winner_delta(T, key);
 }
 
 // Alg. 2 at level l for one pixel, NearestSeed straight from the hash.
@@ -504,10 +484,9 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
     }
     __syncwarp();
 
-    // ---- finer levels over the warp's pixel queue, compacted in place ----
+    // ---- finer levels over the warp's pixel queue, compacted in place: the levels without a
+    //      table (every tabled level had its group pass), NearestSeed from the hash ----
     for (; l >= 1 && n > 0; --l) {
-        const bool table = (l == L - 2 && t2) || (l == L - 1 && t1) || (l == L && t0);
-        const CellGrid& g = (l == L) ? gL : ((l == L - 1) ? gL1 : gL2);
         const uint32_t c_l = level_salt(seed, l);
         int nn = 0;
         for (int k0 = 0; k0 < n; k0 += 32) {
@@ -517,8 +496,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
             if (k < n) {
                 idx = q[k];
                 const int rx = idx & (TW - 1), ry = idx / TW;
-                const uint32_t cand = table ? table_candidate(T, g, l, x0, y0, rx, ry)
-                                            : direct_candidate(a, gtf, x0 + rx, y0 + ry, l, c_l);
+                const uint32_t cand = direct_candidate(a, gtf, x0 + rx, y0 + ry, l, c_l);
                 const uint32_t gp = sm.coord[idx];  // G_T while the pixel is rejected
                 if (accept<EXT>(a, gs, gp, cand)) {
                     sm.coord[idx] = cand;
@@ -539,7 +517,6 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
     if (l == 0) {
         for (int k = lane; k < n; k += 32) {
             const int idx = q[k];
-            const int rx = idx & (TW - 1), ry = idx / TW;
             sm.coord[idx] = __ldg(a.lut + (sm.coord[idx] & a.key_mask));  // the slot holds G_T
             if (LVL) lvl[idx] = 0;
         }
