@@ -293,6 +293,7 @@ def run_ours(args):
             roof_issue = {"bound": "alu", "kernel": dom, "achieved": round(ach_i / 1e9, 1),
                           "peak": round(peak_i / 1e9, 1), "unit": "G warp-instructions/s",
                           "frac": round(ach_i / peak_i, 4), "warp_inst_per_px": round(ipp, 3),
+                          "simt_efficiency": round(tj[key].get("simt_efficiency", 0.0), 4),
                           "peak_source": "SMs x 4 issue slots x max SM clock (B200_PROFILING.md unit counts)"}
     except Exception:
         pass
@@ -335,6 +336,24 @@ def run_ours(args):
                    "step": "stylize (coords + blit colours) with the exact 3-channel table; table built once "
                            "per exemplar (lut3_build_ms, 2^24 entries)"}
         del lut3, ws3
+
+    # ---- level histogram of the headline workload: which level accepted each
+    #      pixel and the mean number of levels a pixel visits (outside any timed region)
+    levels = None
+    if not strip:
+        nf = min(B, 4)
+        prm_l = sb.Params(threshold=cfg["t"], levels=cfg["L"], guide_channels=cfg["C"], seed=cfg["seed"])
+        lv = torch.empty(nf, HT, WT, dtype=torch.uint8, device=dev)
+        sb.stylize_batch(prm_l, cs, gs, lut, gt[:nf], frame_seeds=seeds[:nf], ct=ct[:nf], coords=coords[:nf],
+                         level=lv)
+        hist = torch.bincount(lv.flatten().long(), minlength=cfg["L"] + 1).double()
+        frac = (hist / hist.sum()).tolist()
+        Lc = cfg["L"]
+        visited = sum(f * (Lc - l + 1 if l >= 1 else Lc) for l, f in enumerate(frac))
+        levels = {"accepted_at_level": {str(l): round(frac[l], 4) for l in range(Lc, -1, -1)},
+                  "mean_levels_visited": round(visited, 3), "frames": nf,
+                  "note": "level 0 = no level accepted, LUT look-up (reading R12)"}
+        del lv
 
     # ---- e2e through the host-buffer ABI call (pinned host memory, copies inside timing)
     e2e = None
@@ -408,6 +427,7 @@ def run_ours(args):
         "e2e": e2e,
         "blend_r2": blend,
         "lut_rgb": lut_rgb,
+        "levels": levels,
     }
     return out, rank, world
 

@@ -31,7 +31,9 @@ for row in rows[2:]:
     rd = float(d["dram__bytes_read.sum"]) * scale[unit_r]
     wr = float(d["dram__bytes_write.sum"]) * scale[unit_w]
     inst = float(d["smsp__inst_executed.sum"])
+    tpi = float(d.get("smsp__thread_inst_executed_per_inst_executed.ratio") or 0)
     res[key] = {"dram_read_bytes": rd, "dram_write_bytes": wr, "pixels": px,
-                "bytes_per_px": (rd + wr) / px, "warp_inst_per_px": inst / px, "kernel": name, "report": rep}
+                "bytes_per_px": (rd + wr) / px, "warp_inst_per_px": inst / px,
+                "simt_efficiency": tpi / 32.0, "kernel": name, "report": rep}
 json.dump(res, open(out, "w"), indent=2)
 print(json.dumps(res, indent=2))
