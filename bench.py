@@ -180,6 +180,7 @@ def run_ours(args):
     ct = torch.empty(B, HT, WT, 4, dtype=torch.uint8, device=dev)
     lut = torch.empty(65536, dtype=torch.int32, device=dev)
     lut_ws = torch.empty(65536 * 4, dtype=torch.uint8, device=dev)
+    ex = torch.empty(sb.exemplar_bytes(cs.shape[1], cs.shape[0]), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     p2p = strip and world > 1 and args.gather == "p2p"
     # the C_T buffer the kernels write: local, or (p2p) rank 0's buffer mapped into this rank
@@ -194,16 +195,22 @@ def run_ours(args):
         r_halo = rad if strip else 0
         flags = sb.SB_NO_COLOR if rad > 0 else 0
         prm = sb.Params(threshold=cfg["t"], levels=cfg["L"], blend_radius=0, guide_channels=cfg["C"],
-                        seed=cfg["seed"], flags=flags, row_begin=max(0, rb - r_halo), row_end=min(HT, re_ + r_halo))
-        ev = {k: [] for k in ("lut", "stylize", "vote", "gather")}
+                        seed=cfg["seed"], flags=flags, row_begin=max(0, rb - r_halo), row_end=min(HT, re_ + r_halo),
+                        exemplar=ex)
+        ev = {k: [] for k in ("lut", "exemplar", "stylize", "vote", "gather")}
         launches = [0]
 
         def step(record: bool):
-            es = [torch.cuda.Event(enable_timing=True) for _ in range(5)] if record else None
+            es = [torch.cuda.Event(enable_timing=True) for _ in range(6)] if record else None
             if record:
                 es[0].record(stream)
             sb.build_lut(gs, lut, lut_ws)
             n = sb.launch_count()
+            if record:
+                es[5].record(stream)
+            # the strided exemplar copy (per exemplar, like the LUT): part of every step
+            sb.prepare_exemplar(cs, gs, ex)
+            n += sb.launch_count()
             if record:
                 es[1].record(stream)
             sb.stylize_batch(prm, cs, gs, lut, gt, frame_seeds=seeds, ct=None if rad > 0 else ct_out, coords=coords,
@@ -222,7 +229,8 @@ def run_ours(args):
                 sharding.gather_strips(ct[:, rb:re_], HT, world, rank, dst=0, row_axis=1)
             if record:
                 es[4].record(stream)
-                ev["lut"].append((es[0], es[1]))
+                ev["lut"].append((es[0], es[5]))
+                ev["exemplar"].append((es[5], es[1]))
                 ev["stylize"].append((es[1], es[2]))
                 ev["vote"].append((es[2], es[3]))
                 ev["gather"].append((es[3], es[4]))
@@ -254,7 +262,8 @@ def run_ours(args):
         kt = {k: statistics.mean(a.elapsed_time(b) for a, b in v) for k, v in ev.items()}
         # algorithmic bytes per launch: stylize reads G_T and writes coords (+ C_T
         # when it blits); the vote reads coords and writes C_T
-        alg = {"stylize": (8 if rad > 0 else 12) * px_step, "lut": gs.numel() + 65536 * 4}
+        alg = {"stylize": (8 if rad > 0 else 12) * px_step, "lut": gs.numel() + 65536 * 4,
+               "exemplar": 4 * gs.numel()}
         if rad > 0:
             alg["vote"] = 8 * px_step
         kernels = {k: {"ms_per_launch": round(kt[k], 4), "share": round(kt[k] / ms_step, 4),
@@ -321,7 +330,8 @@ def run_ours(args):
         b3.record(stream)
         torch.cuda.synchronize(dev)
         build_ms = a3.elapsed_time(b3) / 3
-        prm3 = sb.Params(threshold=cfg["t"], levels=cfg["L"], guide_channels=cfg["C"], seed=cfg["seed"], lut_rgb=True)
+        prm3 = sb.Params(threshold=cfg["t"], levels=cfg["L"], guide_channels=cfg["C"], seed=cfg["seed"], lut_rgb=True,
+                         exemplar=ex)
         for _ in range(3):
             sb.stylize_batch(prm3, cs, gs, lut3, gt, frame_seeds=seeds, ct=ct, coords=coords, want_level=False)
         torch.cuda.synchronize(dev)
@@ -364,7 +374,7 @@ def run_ours(args):
         gt_h = gt[:Be].cpu().pin_memory()
         ct_h = torch.empty_like(gt_h).pin_memory()
         prm_e = sb.Params(threshold=cfg["t"], levels=cfg["L"], blend_radius=r, guide_channels=cfg["C"],
-                          seed=cfg["seed"])
+                          seed=cfg["seed"], exemplar=ex)
         depth = int(os.environ.get("SB_E2E_DEPTH", "2"))
         ws_e = sb.host_workspace(WT, HT, r, depth, device=dev)
 
@@ -407,7 +417,7 @@ def run_ours(args):
         "dtype": "u8",
         "data": "synthetic (seeded heightfield-normal 4K frames, sphere-normal exemplar, painted style)",
         "config": {"workload": f"cfg5: {B} x 4K UHD (3840x2160) frames per GPU, 512x512 exemplar, L={cfg['L']}, "
-                               f"t={cfg['t']}, C={cfg['C']}, blend r={r}; step = LUT build + stylize"
+                               f"t={cfg['t']}, C={cfg['C']}, blend r={r}; step = LUT build + strided exemplar copy + stylize"
                                + (" + vote" if r > 0 else " (blit colours)"),
                    "frames_per_gpu": B, "global_frames": B * world, "levels": cfg["L"], "threshold": cfg["t"],
                    "blend_radius": r,

@@ -96,6 +96,13 @@ typedef struct {
      * "segmentation guide which prevents chunks to cross boundaries" of PAPER.md:514-517 --
      * and that byte does not enter e.  (The level-0 look-up ignores labels.)              */
     int32_t  label_channel;
+    /* Optional device pointer (16-byte aligned): the strided exemplar copy written by
+     * sb_prepare_exemplar(cs, gs) for THIS cs/gs.  NULL = read cs and gs directly.  With it,
+     * the exemplar gathers of Alg. 2 line 384 (G_S[s]) and of the blit (C_S[s], line 387) index
+     * the copy with the packed candidate s = x | y<<16 itself; results are identical, only the
+     * address arithmetic per gather is gone.  Used by the tiled kernel for L in 3..5 without
+     * weights/labels; ignored (cs/gs read) elsewhere.                                        */
+    const uint8_t* exemplar;
 } sb_params;
 
 /* Bytes of device workspace sb_build_lut needs (65536 x 4). */
@@ -122,6 +129,20 @@ size_t sb_lut3_workspace_bytes(void);
  *   workspace  device, sb_lut3_workspace_bytes() bytes, scratch (contents undefined after) */
 sb_status sb_build_lut3(const uint8_t* gs, int32_t ws, int32_t hs, uint32_t* lut3,
                         void* workspace, void* stream);
+
+/* Bytes of the strided exemplar copy for a ws x hs exemplar: G_S and C_S, each hs rows of
+ * 2^16 pixels (row stride 256 KiB), i.e. 2 * hs * 2^18 bytes (256 MiB for hs = 512).  Only
+ * ws pixels of a row are written and read; the rest is never touched.  ws <= 32767.        */
+size_t sb_exemplar_bytes(int32_t ws, int32_t hs);
+
+/* The strided exemplar copy used through sb_params.exemplar: exemplar[0 .. hs*2^18) holds
+ * G_S with pixel (x,y) at byte 4*(y*65536 + x), exemplar[hs*2^18 ..) holds C_S the same way,
+ * so a packed source coordinate x | y<<16 is its own pixel index (the two
+ * exemplar gathers of Alg. 2).  Rebuild it whenever cs or gs change (like the LUT).
+ *   cs, gs     device, ws*hs*4: style exemplar C_S and source guide G_S
+ *   exemplar   device, sb_exemplar_bytes(ws, hs) bytes, 16-byte aligned, output           */
+sb_status sb_prepare_exemplar(const uint8_t* cs, const uint8_t* gs, int32_t ws, int32_t hs,
+                              uint8_t* exemplar, void* stream);
 
 /* Alg. 2 for every target pixel, then the vote when prm->blend_radius > 0.
  *   cs, gs     device, ws*hs*4: style exemplar C_S and source guide G_S

@@ -21,7 +21,7 @@ from . import _lib
 from ._lib import SB_JITTER_ZERO, SB_LABEL, SB_LUT_RGB, SB_NO_COLOR, StyleBlitError, check, lib
 
 __all__ = [
-    "Params", "build_lut", "build_lut3", "stylize", "stylize_batch", "vote", "stylize_batch_host", "launch_count",
+    "Params", "build_lut", "build_lut3", "exemplar_bytes", "prepare_exemplar", "stylize", "stylize_batch", "vote", "stylize_batch_host", "launch_count",
     "version", "SB_JITTER_ZERO", "SB_NO_COLOR", "SB_LABEL", "SB_LUT_RGB", "StyleBlitError",
 ]
 
@@ -41,6 +41,7 @@ class Params:
     weights: tuple = (0, 0, 0, 0)  # per-channel integer weights; all zero = unit weights
     label_channel: int | None = None  # segmentation label byte (sets SB_LABEL)
     lut_rgb: bool = False             # `lut` is the 2^24-entry table of build_lut3 (sets SB_LUT_RGB)
+    exemplar: torch.Tensor | None = None  # strided exemplar copy of prepare_exemplar(cs, gs) (speed only)
 
     def c(self) -> _lib.SbParams:
         flags = int(self.flags) | (SB_LABEL if self.label_channel is not None else 0)
@@ -49,7 +50,8 @@ class Params:
         return _lib.SbParams(float(self.threshold), int(self.levels), int(self.blend_radius),
                              int(self.guide_channels), int(self.seed) & 0xFFFFFFFF, flags,
                              int(self.row_begin), int(self.row_end), w,
-                             -1 if self.label_channel is None else int(self.label_channel))
+                             -1 if self.label_channel is None else int(self.label_channel),
+                             None if self.exemplar is None else _dev(self.exemplar, "exemplar", torch.uint8, (1,)))
 
 
 def _dev(t: torch.Tensor, name: str, dtype: torch.dtype, ndim: tuple[int, ...]) -> int:
@@ -104,6 +106,30 @@ def build_lut3(gs: torch.Tensor, lut3: torch.Tensor | None = None, workspace: to
         workspace = torch.empty(lib().sb_lut3_workspace_bytes(), dtype=torch.uint8, device=gs.device)
     check(lib().sb_build_lut3(gs.data_ptr(), ws, hs, lut3.data_ptr(), workspace.data_ptr(), _stream(stream)))
     return lut3
+
+
+def exemplar_bytes(ws: int, hs: int) -> int:
+    """sb_exemplar_bytes: size of the strided exemplar copy (2 * hs * 2^18 bytes)."""
+    return int(lib().sb_exemplar_bytes(int(ws), int(hs)))
+
+
+def prepare_exemplar(cs: torch.Tensor, gs: torch.Tensor, out: torch.Tensor | None = None,
+                     stream=None) -> torch.Tensor:
+    """sb_prepare_exemplar: G_S and C_S copied to rows of 2^16 pixels, so the stylize kernel's
+    exemplar gathers index them with the packed coordinate itself.  Pass
+    the result as Params(exemplar=...); results are identical with and without it."""
+    _dev(cs, "cs", torch.uint8, (3,))
+    _dev(gs, "gs", torch.uint8, (3,))
+    ws, hs = _img_wh(gs, "gs")
+    if _img_wh(cs, "cs") != (ws, hs):
+        raise ValueError("cs and gs must have the same size")
+    if out is None:
+        out = torch.empty(exemplar_bytes(ws, hs), dtype=torch.uint8, device=gs.device)
+    _dev(out, "out", torch.uint8, (1,))
+    if out.numel() < exemplar_bytes(ws, hs):
+        raise ValueError(f"out has {out.numel()} bytes; needs {exemplar_bytes(ws, hs)}")
+    check(lib().sb_prepare_exemplar(cs.data_ptr(), gs.data_ptr(), ws, hs, out.data_ptr(), _stream(stream)))
+    return out
 
 
 def _check_lut(prm: Params, lut: torch.Tensor) -> None:

@@ -23,7 +23,8 @@ SB_MAX_RADIUS = 7
 
 # every symbol include/styleblit.h declares
 EXPORTS = (
-    "sb_lut_workspace_bytes", "sb_build_lut", "sb_lut3_workspace_bytes", "sb_build_lut3", "sb_stylize", "sb_stylize_batch", "sb_vote",
+    "sb_lut_workspace_bytes", "sb_build_lut", "sb_lut3_workspace_bytes", "sb_build_lut3", "sb_exemplar_bytes",
+    "sb_prepare_exemplar", "sb_stylize", "sb_stylize_batch", "sb_vote",
     "sb_host_workspace_bytes", "sb_stylize_batch_host", "sb_last_launch_count",
     "sb_last_error", "sb_version",
 )
@@ -41,6 +42,7 @@ class SbParams(C.Structure):
         ("row_end", C.c_int32),
         ("weights", C.c_uint8 * 4),
         ("label_channel", C.c_int32),
+        ("exemplar", C.c_void_p),
     ]
 
 
@@ -71,6 +73,10 @@ def lib() -> C.CDLL:
     l.sb_lut3_workspace_bytes.argtypes = []
     l.sb_build_lut3.restype = C.c_int
     l.sb_build_lut3.argtypes = [u8p, i32, i32, u32p, vp, vp]
+    l.sb_exemplar_bytes.restype = C.c_size_t
+    l.sb_exemplar_bytes.argtypes = [i32, i32]
+    l.sb_prepare_exemplar.restype = C.c_int
+    l.sb_prepare_exemplar.argtypes = [u8p, u8p, i32, i32, u8p, vp]
     l.sb_stylize.restype = C.c_int
     l.sb_stylize.argtypes = [C.POINTER(SbParams), u8p, u8p, i32, i32, u32p, u8p, i32, i32, u8p, u32p, u8p, vp]
     l.sb_stylize_batch.restype = C.c_int

@@ -89,14 +89,15 @@ sb_status validate(const sb_params* prm, int32_t n_frames, const uint8_t* cs, co
     if (r > 0 && !no_color && !coords) return fail(SB_EINVAL, "coords is NULL but blend_radius=%d needs it", r);
     if (device_outputs) {
         if (!aligned16(cs) || !aligned16(gs) || !aligned16(gt) || (ct && !aligned16(ct)) ||
-            (coords && !aligned16(coords)) || !aligned16(lut))
-            return fail(SB_EINVAL, "image/LUT base pointers must be 16-byte aligned");
+            (coords && !aligned16(coords)) || !aligned16(lut) || (prm->exemplar && !aligned16(prm->exemplar)))
+            return fail(SB_EINVAL, "image/LUT/exemplar base pointers must be 16-byte aligned");
     }
 
     Prepared& p = *out;
     memset(&p, 0, sizeof(p));
     sb::StylizeArgs& a = p.s;
     a.cs = cs; a.gs = gs; a.ws = ws; a.hs = hs; a.lut = lut; a.gt = gt; a.wt = wt; a.ht = ht;
+    a.exemplar = prm->exemplar;
     a.key_mask = (prm->flags & SB_LUT_RGB) ? 0xFFFFFFu : 0xFFFFu;
     a.L = prm->levels;
     const double t2 = std::ceil((double)t * (double)t);  // exact: t is a float (reading R2)
@@ -175,6 +176,26 @@ sb_status sb_build_lut(const uint8_t* gs, int32_t ws, int32_t hs, uint32_t* lut,
         return fail(SB_EINVAL, "gs/lut/workspace must be 16-byte aligned");
     cudaError_t e = sb::launch_build_lut(gs, ws, hs, lut, workspace, (cudaStream_t)stream, &g_launches);
     if (e != cudaSuccess) return cuda_fail(e, "sb_build_lut launch");
+    return SB_OK;
+}
+
+size_t sb_exemplar_bytes(int32_t ws, int32_t hs) {
+    if (ws < 1 || hs < 1 || ws > 32767 || hs > 32767) return 0;
+    return (size_t)2 * (size_t)hs * ((size_t)1 << 18);
+}
+
+sb_status sb_prepare_exemplar(const uint8_t* cs, const uint8_t* gs, int32_t ws, int32_t hs, uint8_t* exemplar,
+                              void* stream) {
+    g_launches = 0;
+    sb_status s;
+    if (!cs) return fail(SB_EINVAL, "cs (style exemplar C_S) is NULL");
+    if (!gs) return fail(SB_EINVAL, "gs (source guide G_S) is NULL");
+    if (!exemplar) return fail(SB_EINVAL, "exemplar is NULL (need sb_exemplar_bytes(ws, hs) bytes)");
+    if ((s = check_dims("source (ws,hs)", ws, hs)) != SB_OK) return s;
+    if (!aligned16(cs) || !aligned16(gs) || !aligned16(exemplar))
+        return fail(SB_EINVAL, "cs/gs/exemplar must be 16-byte aligned");
+    cudaError_t e = sb::launch_prepare_exemplar(cs, gs, ws, hs, exemplar, (cudaStream_t)stream, &g_launches);
+    if (e != cudaSuccess) return cuda_fail(e, "sb_prepare_exemplar launch");
     return SB_OK;
 }
 

@@ -13,6 +13,7 @@ struct StylizeArgs {
     int ws, hs;
     const uint32_t* lut;
     uint32_t key_mask;  // LUT key bits of a guide value: 0xFFFF (2-channel) or 0xFFFFFF (SB_LUT_RGB)
+    const uint8_t* exemplar;  // strided G_S | C_S copy (sb_prepare_exemplar) or NULL
     const uint8_t* gt;  // frame 0 of this launch
     int wt, ht;
     uint8_t* ct;        // NULL: no colour output (SB_NO_COLOR or vote follows)
@@ -48,6 +49,8 @@ cudaError_t launch_build_lut(const uint8_t* gs, int ws, int hs, uint32_t* lut, v
                              cudaStream_t st, int* launches);
 cudaError_t launch_build_lut3(const uint8_t* gs, int ws, int hs, uint32_t* lut3, void* workspace,
                               cudaStream_t st, int* launches);
+cudaError_t launch_prepare_exemplar(const uint8_t* cs, const uint8_t* gs, int ws, int hs, uint8_t* exemplar,
+                                    cudaStream_t st, int* launches);
 cudaError_t launch_stylize_naive(const StylizeArgs& a, int n_frames, cudaStream_t st, int* launches);
 cudaError_t launch_stylize_tiled(const StylizeArgs& a, int n_frames, cudaStream_t st, int* launches);
 cudaError_t launch_vote(const VoteArgs& a, int n_frames, cudaStream_t st, int* launches);

@@ -142,25 +142,27 @@ __device__ __forceinline__ int warp_excl_scan(int v, int* total) {
 // and D = ||G_T[p] - G_S[s]||^2 < T2.  Branch-free: an outside candidate reads G_S[0].
 // G_S gather for the packed candidate c = s.x | s.y<<16 (Alg. 2).  *in: s inside the
 // source (R9; a negative component borrows into a field >= 0x8000 > 32767), tested with one
-// packed 16-bit min against (ws-1 | (hs-1)<<16); the index y*ws + x = c + y*(ws - 65536)
-// (mod 2^32); an outside candidate reads G_S[0].  Branch-free.
+// packed 16-bit min against (ws-1 | (hs-1)<<16).  The index is y*ws + x = c + y*(ws - 65536)
+// (mod 2^32), or, with the strided exemplar copy (PAD: rows of 2^16 pixels), c itself; an
+// outside candidate reads pixel 0.  Branch-free.
+template <bool PAD>
 __device__ __forceinline__ uint32_t gather_gs(const StylizeArgs& a, const uint32_t* __restrict__ gs, uint32_t c,
                                               bool* in) {
     const uint32_t lim = ((uint32_t)(a.hs - 1) << 16) | (uint32_t)(a.ws - 1);
     uint32_t mn;
     asm("min.u16x2 %0, %1, %2;" : "=r"(mn) : "r"(c), "r"(lim));
     *in = mn == c;
-    const uint32_t gi = *in ? c + (c >> 16) * (uint32_t)(a.ws - 65536) : 0u;
+    const uint32_t gi = *in ? (PAD ? c : c + (c >> 16) * (uint32_t)(a.ws - 65536)) : 0u;
     const uint32_t* p;
     asm("mad.wide.u32 %0, %1, 4, %2;" : "=l"(p) : "r"(gi), "l"(gs));
     return __ldg(p);
 }
 
-template <bool EXT>
+template <bool EXT, bool PAD>
 __device__ __forceinline__ bool accept(const StylizeArgs& a, const uint32_t* __restrict__ gs, uint32_t gp,
                                        uint32_t c) {
     bool inb;
-    const uint32_t g = gather_gs(a, gs, c, &inb);
+    const uint32_t g = gather_gs<PAD>(a, gs, c, &inb);
     if (EXT) return inb & guide_ok_ext(gp, g, a.cmask, a.w, a.lmask, a.T2);
     return inb & (guide_d2(gp, g, a.cmask) < a.T2);
 }
@@ -219,7 +221,7 @@ __device__ __forceinline__ uint32_t winner_delta(const Cells& T, uint32_t key) {
 
 // Alg. 2 at level l (h >= 4) for the 4 pixels (px0..px0+3, py) that share one cell.  Writes the
 // 4 packed candidates; returns the acceptance bits.
-template <bool EXT>
+template <bool EXT, bool PAD>
 __device__ __forceinline__ uint32_t group_eval(const Cells& T, const StylizeArgs& a, const uint32_t* __restrict__ gs,
                                                const CellGrid& g, int l, int x0, int y0, int rx0, int ry, uint4 gp4,
                                                uint32_t m, uint32_t cand[4]) {
@@ -235,7 +237,7 @@ __device__ __forceinline__ uint32_t group_eval(const Cells& T, const StylizeArgs
         {
             const uint32_t c = p0 + (uint32_t)i + winner_delta(T, keys[i]);
             cand[i] = c;
-            acc |= (uint32_t)accept<EXT>(a, gs, gpv[i], c) << i;
+            acc |= (uint32_t)accept<EXT, PAD>(a, gs, gpv[i], c) << i;
         }
     }
     return acc;
@@ -281,8 +283,9 @@ __device__ __forceinline__ uint32_t direct_candidate(const StylizeArgs& a, const
 }  // namespace
 
 // LT > 0: the hierarchy depth as a compile-time constant (the common depths; all level geometry
-// folds), LT = 0: a.L at run time.
-template <bool EXT, bool LVL, int LT>
+// folds), LT = 0: a.L at run time.  PAD: the exemplar gathers index the strided copy
+// a.exemplar (sb_prepare_exemplar) with the packed coordinate itself.
+template <bool EXT, bool LVL, int LT, bool PAD>
 __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_constant__ StylizeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -300,7 +303,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
     const int frame = blockIdx.z;
     const int64_t fpx = (int64_t)a.wt * a.ht;
     const uint32_t* __restrict__ gtf = reinterpret_cast<const uint32_t*>(a.gt) + fpx * frame;
-    const uint32_t* __restrict__ gs = reinterpret_cast<const uint32_t*>(a.gs);
+    const uint32_t* __restrict__ gs = reinterpret_cast<const uint32_t*>(PAD ? a.exemplar : a.gs);
     const uint32_t seed = a.frame_seed(frame);
     const uint32_t wt = (uint32_t)a.wt;
 
@@ -364,7 +367,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                 for (int i = 0; i < 4; ++i) {
                     cand[i] = p0 + (uint32_t)i + winner_delta(T, key[j][i]);
                     bool in;
-                    gv[i] = gather_gs(a, gs, cand[i], &in);
+                    gv[i] = gather_gs<PAD>(a, gs, cand[i], &in);
                     inb |= (uint32_t)in << i;
                 }
             }
@@ -417,7 +420,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                     // the group's slots: coords of its accepted pixels, G_T of the rejected (m)
                     uint4 cv = *reinterpret_cast<const uint4*>(&sm.coord[pbase]);
                     uint32_t cand[4];
-                    const uint32_t acc = group_eval<EXT>(T, a, gs, g, lp, x0, y0, grx0, ry, cv, m, cand);
+                    const uint32_t acc = group_eval<EXT, PAD>(T, a, gs, g, lp, x0, y0, grx0, ry, cv, m, cand);
                     // merge the newly accepted pixels: one 16-byte read-modify-write instead of
                     // four conflicting scalar stores
                     const uint32_t take = m & acc;
@@ -498,7 +501,7 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
                 const int rx = idx & (TW - 1), ry = idx / TW;
                 const uint32_t cand = direct_candidate(a, gtf, x0 + rx, y0 + ry, l, c_l);
                 const uint32_t gp = sm.coord[idx];  // G_T while the pixel is rejected
-                if (accept<EXT>(a, gs, gp, cand)) {
+                if (accept<EXT, PAD>(a, gs, gp, cand)) {
                     sm.coord[idx] = cand;
                     if (LVL) lvl[idx] = (uint8_t)l;
                 } else {
@@ -524,7 +527,8 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
     __syncwarp();
 
     // ---- outputs: coords, levels, blit colours ----
-    const uint32_t* __restrict__ cs = reinterpret_cast<const uint32_t*>(a.cs);
+    const uint32_t* __restrict__ cs = reinterpret_cast<const uint32_t*>(
+        PAD ? a.exemplar + (size_t)a.hs * ((size_t)1 << 18) : a.cs);
     const uint32_t ws = (uint32_t)a.ws;
 #pragma unroll 2
     for (int j = 0; j < RPW; ++j) {
@@ -536,10 +540,12 @@ __global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_const
         if (a.level) st_cs_u32(a.level + o, *reinterpret_cast<const uint32_t*>(&lvl[ry * TW + rx0]));
         if (a.ct) {
             uint4 col;
-            col.x = __ldg(cs + ((cv.x >> 16) * ws + (cv.x & 0xFFFFu)));
-            col.y = __ldg(cs + ((cv.y >> 16) * ws + (cv.y & 0xFFFFu)));
-            col.z = __ldg(cs + ((cv.z >> 16) * ws + (cv.z & 0xFFFFu)));
-            col.w = __ldg(cs + ((cv.w >> 16) * ws + (cv.w & 0xFFFFu)));
+            // packed x | y<<16 -> pixel index y*ws + x (PAD: the packed value itself)
+            auto idx = [&](uint32_t c) { return PAD ? c : (c >> 16) * ws + (c & 0xFFFFu); };
+            col.x = __ldg(cs + idx(cv.x));
+            col.y = __ldg(cs + idx(cv.y));
+            col.z = __ldg(cs + idx(cv.z));
+            col.w = __ldg(cs + idx(cv.w));
             st_cs_u4(a.ct + 4 * o, col);
         }
     }
@@ -549,14 +555,19 @@ cudaError_t launch_stylize_tiled(const StylizeArgs& a, int n_frames, cudaStream_
     // tables sized for this L; the level map only when requested
     const size_t smem = sizeof(Smem) + (size_t)table_cells(a.L) * (sizeof(uint2) + sizeof(int2)) + (a.level ? TP : 0);
     void (*kern)(StylizeArgs);
+    const bool pad = a.exemplar != nullptr;  // the strided exemplar copy: L in 3..5, no weights/labels
     if (a.ext) {
-        kern = a.level ? stylize_tiled_kernel<true, true, 0> : stylize_tiled_kernel<true, false, 0>;
+        kern = a.level ? stylize_tiled_kernel<true, true, 0, false> : stylize_tiled_kernel<true, false, 0, false>;
     } else if (a.level) {
-        kern = a.L == 5 ? stylize_tiled_kernel<false, true, 5> : a.L == 4 ? stylize_tiled_kernel<false, true, 4>
-             : a.L == 3 ? stylize_tiled_kernel<false, true, 3> : stylize_tiled_kernel<false, true, 0>;
+        kern = a.L == 5 ? (pad ? stylize_tiled_kernel<false, true, 5, true> : stylize_tiled_kernel<false, true, 5, false>)
+             : a.L == 4 ? (pad ? stylize_tiled_kernel<false, true, 4, true> : stylize_tiled_kernel<false, true, 4, false>)
+             : a.L == 3 ? (pad ? stylize_tiled_kernel<false, true, 3, true> : stylize_tiled_kernel<false, true, 3, false>)
+                        : stylize_tiled_kernel<false, true, 0, false>;
     } else {
-        kern = a.L == 5 ? stylize_tiled_kernel<false, false, 5> : a.L == 4 ? stylize_tiled_kernel<false, false, 4>
-             : a.L == 3 ? stylize_tiled_kernel<false, false, 3> : stylize_tiled_kernel<false, false, 0>;
+        kern = a.L == 5 ? (pad ? stylize_tiled_kernel<false, false, 5, true> : stylize_tiled_kernel<false, false, 5, false>)
+             : a.L == 4 ? (pad ? stylize_tiled_kernel<false, false, 4, true> : stylize_tiled_kernel<false, false, 4, false>)
+             : a.L == 3 ? (pad ? stylize_tiled_kernel<false, false, 3, true> : stylize_tiled_kernel<false, false, 3, false>)
+                        : stylize_tiled_kernel<false, false, 0, false>;
     }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -129,6 +129,21 @@ def test_build_lut3_invalid(lib):
     assert lib.sb_build_lut3(FAKE, 4, 40000, FAKE, FAKE, None) == _lib.SB_EINVAL
 
 
+def test_exemplar_copy_abi(lib):
+    assert lib.sb_exemplar_bytes(512, 512) == 2 * 512 * (1 << 18)
+    assert lib.sb_exemplar_bytes(37, 29) == 2 * 29 * (1 << 18)
+    assert lib.sb_exemplar_bytes(0, 5) == 0 and lib.sb_exemplar_bytes(40000, 5) == 0
+    assert lib.sb_prepare_exemplar(FAKE, FAKE, 4, 4, 0, None) == _lib.SB_EINVAL
+    assert "sb_exemplar_bytes" in lib.sb_last_error().decode()
+    assert lib.sb_prepare_exemplar(0, FAKE, 4, 4, FAKE, None) == _lib.SB_EINVAL
+    assert lib.sb_prepare_exemplar(FAKE, FAKE, 4, 4, FAKE + 4, None) == _lib.SB_EINVAL
+    assert "aligned" in lib.sb_last_error().decode()
+    p = _prm()
+    p.exemplar = FAKE + 8   # misaligned strided copy is refused before any launch
+    st = lib.sb_stylize(C.byref(p), FAKE, FAKE, 64, 64, FAKE, FAKE, 64, 64, FAKE, 0, 0, None)
+    assert st == _lib.SB_EINVAL and "exemplar" in lib.sb_last_error().decode()
+
+
 def test_host_batch_invalid(lib):
     p = _prm()
     st = lib.sb_stylize_batch_host(C.byref(p), 1, None, FAKE, FAKE, 64, 64, FAKE, FAKE, 64, 64, FAKE, 0, FAKE, 16, 2,

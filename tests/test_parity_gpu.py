@@ -38,7 +38,12 @@ def run_both(prm: sb.Params, cs, gs, gt, want_vote=True):
     csd, gsd, gtd = cs.to(DEV), gs.to(DEV), gt.to(DEV)
     lut_d = sb.build_lut(gsd)
     ct, coords, level = sb.stylize(prm, csd, gsd, lut_d, gtd)
+    # the strided exemplar copy (sb_prepare_exemplar) is a speed option: identical results
+    ex = sb.prepare_exemplar(csd, gsd)
+    ct2, coords2, level2 = sb.stylize(sb.Params(**{**prm.__dict__, "exemplar": ex}), csd, gsd, lut_d, gtd)
     torch.cuda.synchronize()
+    assert torch.equal(coords, coords2) and torch.equal(level, level2), "exemplar copy changed coords/levels"
+    assert (ct is None and ct2 is None) or torch.equal(ct, ct2), "exemplar copy changed colours"
     csn, gsn, gtn = cs.numpy(), gs.numpy(), gt.numpy()
     lut = oracle_lut(gsn)
     oprm = oracle.Params(t=prm.threshold, L=prm.levels, C=prm.guide_channels, seed=prm.seed,
@@ -417,3 +422,37 @@ def test_batch_longer_than_one_launch():
         o = oracle.stylize(oracle.Params(t=cfg["t"], L=3, C=3, seed=seeds[i]), cs.numpy(), gs.numpy(), lut,
                            frames[i].numpy())
         assert (u32(co[i]) == o[1]).all() and (lv[i].cpu().numpy() == o[2]).all(), i
+
+
+# ------------------------------------------------------------------ strided exemplar copy
+def test_prepare_exemplar_layout():
+    """sb_prepare_exemplar: G_S then C_S, each hs rows of 2^16 pixels (include/styleblit.h)."""
+    cs, gs, _ = _rand_case(8, 8, 37, 29, seed=3)   # ws not a multiple of 4
+    csd, gsd = cs.to(DEV), gs.to(DEV)
+    ex = sb.prepare_exemplar(csd, gsd)
+    assert ex.numel() == 2 * 29 * (1 << 18)
+    rows = ex.view(2, 29, 65536, 4)[:, :, :37, :].cpu()
+    assert torch.equal(rows[0], gs) and torch.equal(rows[1], cs)
+
+
+@pytest.mark.parametrize("L", [3, 4, 5])
+def test_exemplar_copy_batch_and_strips(L):
+    """With the strided exemplar copy: a batch with per-frame seeds and row strips equal the
+    oracle / the whole-frame result (the kernels that use it: L = 3..5)."""
+    cfg = synth.CONFIGS[3]
+    cs, gs = [t.to(DEV) for t in synth.exemplar(cfg)]
+    lut = sb.build_lut(gs)
+    ex = sb.prepare_exemplar(cs, gs)
+    frames = torch.stack([synth.heightfield_normals(260, 70, seed=5, frame=i) for i in range(3)]).to(DEV)
+    prm = sb.Params(threshold=cfg["t"], levels=L, guide_channels=3, seed=11, exemplar=ex)
+    ct, co, lv = sb.stylize_batch(prm, cs, gs, lut, frames)
+    lutn = oracle_lut(gs.cpu().numpy())
+    for i in range(3):
+        o = oracle.stylize(oracle.Params(t=cfg["t"], L=L, C=3, seed=11 + i), cs.cpu().numpy(), gs.cpu().numpy(), lutn,
+                           frames[i].cpu().numpy(), nthreads=NTH)
+        assert (u32(co[i]) == o[1]).all() and (lv[i].cpu().numpy() == o[2]).all() and (ct[i].cpu().numpy() == o[0]).all()
+    ct2 = torch.zeros_like(ct[0])
+    for a, b in zip([0, 3, 37, 70][:-1], [0, 3, 37, 70][1:]):
+        sb.stylize(sb.Params(**{**prm.__dict__, "seed": 11, "row_begin": a, "row_end": b}), cs, gs, lut, frames[0],
+                   ct=ct2)
+    assert torch.equal(ct2, ct[0])
