@@ -219,7 +219,7 @@ def run_ours(args):
             if record:
                 es[2].record(stream)
             if rad > 0:
-                sb.vote(coords, cs, rad, ct=ct_out, row_begin=rb, row_end=re_)
+                sb.vote(coords, cs, rad, ct=ct_out, row_begin=rb, row_end=re_, exemplar=ex)
                 n += sb.launch_count()
             if record:
                 es[3].record(stream)

@@ -98,10 +98,10 @@ typedef struct {
     int32_t  label_channel;
     /* Optional device pointer (16-byte aligned): the strided exemplar copy written by
      * sb_prepare_exemplar(cs, gs) for THIS cs/gs.  NULL = read cs and gs directly.  With it,
-     * the exemplar gathers of Alg. 2 line 384 (G_S[s]) and of the blit (C_S[s], line 387) index
-     * the copy with the packed candidate s = x | y<<16 itself; results are identical, only the
-     * address arithmetic per gather is gone.  Used by the tiled kernel for L in 3..5 without
-     * weights/labels; ignored (cs/gs read) elsewhere.                                        */
+     * the exemplar gathers of Alg. 2 line 384 (G_S[s]), of the blit (C_S[s], line 387) and of
+     * the vote index the copy with the packed coordinate x | y<<16 itself; results are
+     * identical, only the address arithmetic per gather is gone.  Used by the tiled stylize
+     * kernel for L in 3..5 without weights/labels and by the vote; ignored elsewhere.      */
     const uint8_t* exemplar;
 } sb_params;
 
@@ -175,10 +175,13 @@ sb_status sb_stylize_batch(const sb_params* prm, int32_t n_frames, const uint32_
  *   cs         device, ws*hs*4, style exemplar C_S
  *   r          voting radius, 0..SB_MAX_RADIUS (0 = blit)
  *   ct         device, n_frames*wt*ht*4, output; only rows [row_begin, row_end) are written
- *              (0,0 = all rows); coords rows [row_begin - r, row_end + r) are read.       */
+ *              (0,0 = all rows); coords rows [row_begin - r, row_end + r) are read.
+ *   exemplar   NULL, or the strided copy of sb_prepare_exemplar for this cs (speed only:
+ *              the colour gathers then index it with packed coordinates; same results)     */
 sb_status sb_vote(const uint32_t* coords, int32_t n_frames, int32_t wt, int32_t ht,
                   const uint8_t* cs, int32_t ws, int32_t hs, int32_t r,
-                  uint8_t* ct, int32_t row_begin, int32_t row_end, void* stream);
+                  uint8_t* ct, int32_t row_begin, int32_t row_end, const uint8_t* exemplar,
+                  void* stream);
 
 /* Bytes of device workspace sb_stylize_batch_host needs for frames of wt x ht with
  * `depth` frames in flight per stage (2 = double buffering). */

@@ -192,8 +192,9 @@ def stylize_batch(prm: Params, cs: torch.Tensor, gs: torch.Tensor, lut: torch.Te
 
 
 def vote(coords: torch.Tensor, cs: torch.Tensor, r: int, ct: torch.Tensor | None = None,
-         row_begin: int = 0, row_end: int = 0, stream=None) -> torch.Tensor:
-    """sb_vote: C_T from a coordinate field.  coords [H,W] or [N,H,W] int32."""
+         row_begin: int = 0, row_end: int = 0, exemplar: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """sb_vote: C_T from a coordinate field.  coords [H,W] or [N,H,W] int32.
+    exemplar: optional strided copy from prepare_exemplar(cs, gs) (speed only)."""
     squeeze = coords.dim() == 2
     co = coords.unsqueeze(0) if squeeze else coords
     _dev(co, "coords", torch.int32, (3,))
@@ -205,8 +206,9 @@ def vote(coords: torch.Tensor, cs: torch.Tensor, r: int, ct: torch.Tensor | None
     elif squeeze:
         ct = ct.unsqueeze(0)
     _dev(ct, "ct", torch.uint8, (4,))
+    ex = None if exemplar is None else _dev(exemplar, "exemplar", torch.uint8, (1,))
     check(lib().sb_vote(co.data_ptr(), n, wt, ht, cs.data_ptr(), ws, hs, int(r), ct.data_ptr(), int(row_begin),
-                        int(row_end), _stream(stream)))
+                        int(row_end), ex, _stream(stream)))
     return ct[0] if squeeze else ct
 
 

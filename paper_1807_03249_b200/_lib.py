@@ -83,7 +83,7 @@ def lib() -> C.CDLL:
     l.sb_stylize_batch.argtypes = [C.POINTER(SbParams), i32, C.POINTER(C.c_uint32), u8p, u8p, i32, i32, u32p, u8p,
                                    i32, i32, u8p, u32p, u8p, vp]
     l.sb_vote.restype = C.c_int
-    l.sb_vote.argtypes = [u32p, i32, i32, i32, u8p, i32, i32, i32, u8p, i32, i32, vp]
+    l.sb_vote.argtypes = [u32p, i32, i32, i32, u8p, i32, i32, i32, u8p, i32, i32, u8p, vp]
     l.sb_host_workspace_bytes.restype = C.c_size_t
     l.sb_host_workspace_bytes.argtypes = [i32, i32, i32, i32]
     l.sb_stylize_batch_host.restype = C.c_int

@@ -126,6 +126,7 @@ sb_status validate(const sb_params* prm, int32_t n_frames, const uint8_t* cs, co
     if (p.vote) {
         sb::VoteArgs& v = p.v;
         v.coords = coords; v.cs = cs; v.ws = ws; v.hs = hs; v.wt = wt; v.ht = ht; v.r = r; v.ct = ct;
+        v.cs_pad = prm->exemplar ? prm->exemplar + (size_t)hs * ((size_t)1 << 18) : nullptr;
         v.row_begin = rb; v.row_end = re;
     }
     return SB_OK;
@@ -234,7 +235,8 @@ sb_status sb_stylize_batch(const sb_params* prm, int32_t n_frames, const uint32_
 }
 
 sb_status sb_vote(const uint32_t* coords, int32_t n_frames, int32_t wt, int32_t ht, const uint8_t* cs, int32_t ws,
-                  int32_t hs, int32_t r, uint8_t* ct, int32_t row_begin, int32_t row_end, void* stream) {
+                  int32_t hs, int32_t r, uint8_t* ct, int32_t row_begin, int32_t row_end, const uint8_t* exemplar,
+                  void* stream) {
     g_launches = 0;
     sb_status s;
     if (!coords) return fail(SB_EINVAL, "coords is NULL");
@@ -248,14 +250,15 @@ sb_status sb_vote(const uint32_t* coords, int32_t n_frames, int32_t wt, int32_t 
     if (row_begin < 0 || row_end > ht || row_begin >= row_end)
         return fail(SB_EINVAL, "rows [row_begin=%d,row_end=%d) not a non-empty range inside [0,%d)", row_begin, row_end,
                     ht);
-    if (!aligned16(coords) || !aligned16(cs) || !aligned16(ct))
-        return fail(SB_EINVAL, "coords/cs/ct must be 16-byte aligned");
+    if (!aligned16(coords) || !aligned16(cs) || !aligned16(ct) || (exemplar && !aligned16(exemplar)))
+        return fail(SB_EINVAL, "coords/cs/ct/exemplar must be 16-byte aligned");
     if (wt % 4 != 0) return fail(SB_EUNSUPPORTED, "sb_vote needs wt %% 4 == 0 (got %d); use sb_stylize", wt);
     const int64_t fpx = (int64_t)wt * ht;
     for (int f0 = 0; f0 < n_frames; f0 += 65535) {
         const int nf = (n_frames - f0) < 65535 ? (n_frames - f0) : 65535;
         sb::VoteArgs v;
         v.coords = coords + fpx * f0; v.cs = cs; v.ws = ws; v.hs = hs; v.wt = wt; v.ht = ht; v.r = r;
+        v.cs_pad = exemplar ? exemplar + (size_t)hs * ((size_t)1 << 18) : nullptr;
         v.ct = ct + 4 * fpx * f0; v.row_begin = row_begin; v.row_end = row_end;
         cudaError_t e = sb::launch_vote(v, nf, (cudaStream_t)stream, &g_launches);
         if (e != cudaSuccess) return cuda_fail(e, "vote launch");

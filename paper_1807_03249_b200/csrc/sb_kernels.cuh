@@ -38,6 +38,7 @@ struct StylizeArgs {
 struct VoteArgs {
     const uint32_t* coords;  // frame 0 of this launch
     const uint8_t* cs;
+    const uint8_t* cs_pad;   // C_S in the strided exemplar copy (rows of 2^16 pixels) or NULL
     int ws, hs;
     int wt, ht;
     int r;

@@ -78,7 +78,10 @@ __device__ __forceinline__ void swar_add(uint32_t c, uint32_t& lo, uint32_t& hi)
 }
 }  // namespace
 
-template <int R>
+// PAD: C_S is read from the strided exemplar copy (rows of 2^16 pixels, sb_prepare_exemplar),
+// where a packed coordinate x | y<<16 is its own index: the "linear" source indices below are
+// then the packed values themselves (row stride 65536) and the conversion pass disappears.
+template <int R, bool PAD>
 __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteArgs a) {
     constexpr int SW = TW + 2 * R, SH = TH + 2 * R;
     constexpr int KR = (R + 3) / 4;           // 16-byte words covering the halo
@@ -97,9 +100,10 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteAr
     const int y0 = a.row_begin + (blockIdx.x / tiles_x) * TH;
     const int64_t fpx = (int64_t)a.wt * a.ht;
     const uint32_t* __restrict__ cf = a.coords + fpx * blockIdx.y;
-    const uint32_t* __restrict__ cs = reinterpret_cast<const uint32_t*>(a.cs);
+    const uint32_t* __restrict__ cs = reinterpret_cast<const uint32_t*>(PAD ? a.cs_pad : a.cs);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t ws = (uint32_t)a.ws, hs = (uint32_t)a.hs;
+    const uint32_t wsl = PAD ? 65536u : ws;  // row stride of the "linear" source index
 
     if (threadIdx.x == 0) qn = qn3 = 0;
     // ---- stage coords (tile + halo), outside the target -> kOutside; test the fast-tile margin
@@ -161,8 +165,8 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteAr
     const int g = lane;                  // this thread's 4-pixel group column (pixels 4g..4g+3)
     if (fast) {
         // ---- packed -> linear source index, in place (16 bytes at a time; the unused
-        //      padding words are converted too, harmlessly)
-        for (int i = threadIdx.x; i < SH * (SWP / 4); i += NT) {
+        //      padding words are converted too, harmlessly); with PAD the packed value is it
+        if (!PAD) for (int i = threadIdx.x; i < SH * (SWP / 4); i += NT) {
             const int yy = i / (SWP / 4), c4 = i - yy * (SWP / 4);
             uint4 v = *reinterpret_cast<const uint4*>(&sc[yy][4 * c4]);
             v.x = (v.x >> 16) * ws + (v.x & 0xFFFFu);
@@ -171,7 +175,7 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteAr
             v.w = (v.w >> 16) * ws + (v.w & 0xFFFFu);
             *reinterpret_cast<uint4*>(&sc[yy][4 * c4]) = v;
         }
-        __syncthreads();
+        if (!PAD) __syncthreads();
         if (R > 0) {
             // ---- 1. row-segment nibbles: tile columns 4g-R .. 4g+3+R of staged row yy
             for (int e = threadIdx.x; e < SH * NG; e += NT) {
@@ -223,7 +227,7 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteAr
                 cx3 |= seg3[ry + R + j][g];
                 const uint4 v4 = *reinterpret_cast<const uint4*>(&sc[ry + R + j][OFF + 4 * g]);
                 const uint32_t vv[4] = {v4.x, v4.y, v4.z, v4.w};
-                const uint32_t sh = (uint32_t)j * ws;
+                const uint32_t sh = (uint32_t)j * wsl;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) m &= ~((uint32_t)(vv[k] != cp[k] + sh) << k);
                 uni &= (R > 0) ? m : 0xFu;
@@ -287,7 +291,7 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteAr
                 const uint32_t c1 = m ? (uint32_t)__ffs(m) : W;      // length of run 1
                 const uint32_t h2 = c1 < W ? c1 : 0u;                // head of run 2 (or any)
                 const uint32_t* row = &sc[yy][OFF + x - R];
-                const uint32_t shy = (uint32_t)dy * ws;
+                const uint32_t shy = (uint32_t)dy * wsl;
                 const uint32_t col1 = __ldg(cs + (row[0] - shy + (uint32_t)R));
                 const uint32_t c2 = W - c1;
                 const uint32_t col2 = ldg_if(cs + (row[h2] - shy - (h2 - (uint32_t)R)), c2 != 0);
@@ -309,7 +313,7 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteAr
                 const uint32_t bits = __funnelshift_r(hl[yy][b >> 5], hl[yy][(b >> 5) + 1], b & 31u);
                 uint32_t m = ~bits & ((1u << (2 * R)) - 1u);  // bit i: a run ends at window position i
                 const uint32_t* row = &sc[yy][OFF + x - R];
-                const uint32_t shy = (uint32_t)dy * ws;
+                const uint32_t shy = (uint32_t)dy * wsl;
                 uint32_t start = 0;
                 uint32_t pos = row[0] - shy + (uint32_t)R;
                 while (m) {
@@ -345,7 +349,7 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteAr
                     const uint32_t w = sc[ry + R + dy][OFF + x + dx];
                     const uint32_t pos = w - (uint32_t)dx - sh;
                     const bool in = (w != kOutside) & ((pos & 0xFFFFu) < ws) & ((pos >> 16) < hs);
-                    const uint32_t c = __ldg(cs + (in ? (pos >> 16) * ws + (pos & 0xFFFFu) : 0u));
+                    const uint32_t c = __ldg(cs + (in ? (PAD ? pos : (pos >> 16) * ws + (pos & 0xFFFFu)) : 0u));
                     if (in) { swar_add(c, lo, hi); ++cnt; }
                 }
             }
@@ -387,9 +391,10 @@ static int vote_carveout() {
 
 template <int R>
 static void launch_r(const VoteArgs& a, dim3 grid, cudaStream_t st) {
+    auto kern = a.cs_pad ? vote_kernel<R, true> : vote_kernel<R, false>;
     if (vote_carveout() >= 0)
-        cudaFuncSetAttribute(vote_kernel<R>, cudaFuncAttributePreferredSharedMemoryCarveout, vote_carveout());
-    vote_kernel<R><<<grid, NT, 0, st>>>(a);
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, vote_carveout());
+    kern<<<grid, NT, 0, st>>>(a);
 }
 
 cudaError_t launch_vote(const VoteArgs& a, int n_frames, cudaStream_t st, int* launches) {

@@ -456,3 +456,28 @@ def test_exemplar_copy_batch_and_strips(L):
         sb.stylize(sb.Params(**{**prm.__dict__, "seed": 11, "row_begin": a, "row_end": b}), cs, gs, lut, frames[0],
                    ct=ct2)
     assert torch.equal(ct2, ct[0])
+
+
+@pytest.mark.parametrize("r", [1, 2, 3])
+def test_vote_exemplar_copy(r):
+    """sb_vote with the strided exemplar copy equals sb_vote without it and the oracle, on a
+    coordinate field with chunk seams, frame borders and sources at the exemplar border."""
+    rng = np.random.RandomState(r)
+    ws, hs, wt, ht = 61, 47, 264, 40
+    cs = torch.from_numpy(rng.randint(0, 256, (hs, ws, 4)).astype(np.uint8))
+    gs = torch.from_numpy(rng.randint(0, 256, (hs, ws, 4)).astype(np.uint8))
+    # chunked field: 8x8 chunks copying random source blocks (some touching the source border)
+    yy, xx = np.mgrid[0:ht, 0:wt]
+    ox = rng.randint(-10, ws - 2, (ht // 8 + 1, wt // 8 + 1))
+    oy = rng.randint(-10, hs - 2, (ht // 8 + 1, wt // 8 + 1))
+    sx = np.clip(xx % 8 + ox[yy // 8, xx // 8], 0, ws - 1)
+    sy = np.clip(yy % 8 + oy[yy // 8, xx // 8], 0, hs - 1)
+    co = (sx | (sy << 16)).astype(np.uint32)
+    csd, gsd = cs.to(DEV), gs.to(DEV)
+    cod = torch.from_numpy(co.view(np.int32)).to(DEV)
+    ex = sb.prepare_exemplar(csd, gsd)
+    a = sb.vote(cod, csd, r)
+    b = sb.vote(cod, csd, r, exemplar=ex)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    assert (b.cpu().numpy() == oracle.vote(co, cs.numpy(), r, nthreads=NTH)).all()
