@@ -366,20 +366,22 @@ def run_ours(args):
         del lv
 
     # ---- e2e through the host-buffer ABI call (pinned host memory, copies inside timing)
-    e2e = None
-    if not args.no_e2e and args.e2e_steps > 0 and not strip:
+    def run_e2e(rgb: bool):
         # the step's whole batch through host memory (fill/drain of the copy pipeline amortised
-        # over the batch); SB_E2E_FRAMES caps it (pinned host memory: 2 x 33 MB per frame)
+        # over the batch); SB_E2E_FRAMES caps it (pinned host memory: 2 x 33 MB per frame).
+        # rgb: the packed-RGB host frames of SB_HOST_RGB (3 bytes per pixel each way; C = 3).
         Be = min(B, int(os.environ.get("SB_E2E_FRAMES", "64")))
-        gt_h = gt[:Be].cpu().pin_memory()
+        ch = 3 if rgb else 4
+        gt_h = gt[:Be, ..., :ch].contiguous().cpu().pin_memory()
         ct_h = torch.empty_like(gt_h).pin_memory()
         prm_e = sb.Params(threshold=cfg["t"], levels=cfg["L"], blend_radius=r, guide_channels=cfg["C"],
-                          seed=cfg["seed"], exemplar=ex)
+                          seed=cfg["seed"], exemplar=ex, flags=sb.SB_HOST_RGB if rgb else 0)
         depth = int(os.environ.get("SB_E2E_DEPTH", "2"))
         ws_e = sb.host_workspace(WT, HT, r, depth, device=dev)
 
         def e2e_step():
             sb.build_lut(gs, lut, lut_ws)
+            sb.prepare_exemplar(cs, gs, ex)
             sb.stylize_batch_host(prm_e, cs, gs, lut, gt_h, ct_h, frame_seeds=seeds[:Be], workspace=ws_e, depth=depth)
 
         e2e_step()
@@ -397,10 +399,19 @@ def run_ours(args):
             tt = torch.tensor([ems], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ems = float(tt.item())
-        e2e = {"value": round(world * Be * WT * HT / (ems * 1e-3) / 1e6, 1), "unit": "MP/s",
-               "h2d_bytes_per_step": Be * WT * HT * 4, "d2h_bytes_per_step": Be * WT * HT * 4,
+        res = {"value": round(world * Be * WT * HT / (ems * 1e-3) / 1e6, 1), "unit": "MP/s",
+               "h2d_bytes_per_step": Be * WT * HT * ch, "d2h_bytes_per_step": Be * WT * HT * ch,
                "frames_per_step": Be, "ms_per_step": round(ems, 3),
-               "api": f"sb_stylize_batch_host (pinned host G_T in, pinned host C_T out, {depth}-deep copy/compute pipeline)"}
+               "api": (f"sb_stylize_batch_host (pinned host G_T in, pinned host C_T out, {depth}-deep copy/compute "
+                       "pipeline" + ("; SB_HOST_RGB: packed RGB frames, C_T channels 0..2)" if rgb else ")"))}
+        del gt_h, ct_h, ws_e
+        return res
+
+    e2e = e2e_rgb = None
+    if not args.no_e2e and args.e2e_steps > 0 and not strip:
+        e2e = run_e2e(False)
+        if cfg["C"] <= 3:
+            e2e_rgb = run_e2e(True)
 
     # ---- parity spot check of this run's outputs (sampled pixels of frame 0 vs oracle) is in tests/.
     out = {
@@ -435,6 +446,7 @@ def run_ours(args):
         "gpu_launches": main["launches"],
         "clocks": main["clocks"],
         "e2e": e2e,
+        "e2e_rgb": e2e_rgb,
         "blend_r2": blend,
         "lut_rgb": lut_rgb,
         "levels": levels,

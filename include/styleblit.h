@@ -60,6 +60,11 @@ typedef enum {
 #define SB_LUT_RGB     0x8u  /* `lut` is the exact 3-channel table of sb_build_lut3 (2^24
                                 entries, key G[0] | G[1]<<8 | G[2]<<16) instead of the
                                 2-channel table                                            */
+#define SB_HOST_RGB   0x10u  /* sb_stylize_batch_host only: the HOST frames are packed 3 bytes
+                                per pixel -- gt_host holds guide channels 0..2 (channel 3 is
+                                taken as 0; needs guide_channels <= 3 and no label in byte 3)
+                                and ct_host receives C_T channels 0..2 -- so 3/4 of the PCIe
+                                bytes move; the device kernels unpack/pack them.  wt % 4 == 0. */
 
 #define SB_MAX_LEVELS 12      /* level l uses spacing h = 2^l, l in [1, SB_MAX_LEVELS]       */
 #define SB_MAX_RADIUS 7       /* voting radius r in [0, SB_MAX_RADIUS]; (2r+1)^2*255 < 2^16   */
@@ -188,7 +193,8 @@ sb_status sb_vote(const uint32_t* coords, int32_t n_frames, int32_t wt, int32_t 
 size_t sb_host_workspace_bytes(int32_t wt, int32_t ht, int32_t blend_radius, int32_t depth);
 
 /* sb_stylize_batch with HOST frame buffers: gt_host (n_frames*wt*ht*4, input) and
- * ct_host (same size, output) are host memory (pinned for full copy bandwidth); cs, gs,
+ * ct_host (same size, output; 3 bytes per pixel each with SB_HOST_RGB) are host memory
+ * (pinned for full copy bandwidth); cs, gs,
  * lut and workspace are device memory.  Frames stream through `depth` device slots:
  * host->device copy of frame i+1, compute of frame i and device->host copy of frame i-1
  * overlap on the library's own streams, ordered after `stream`.  Returns when ct_host

@@ -18,11 +18,11 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import SB_JITTER_ZERO, SB_LABEL, SB_LUT_RGB, SB_NO_COLOR, StyleBlitError, check, lib
+from ._lib import SB_HOST_RGB, SB_JITTER_ZERO, SB_LABEL, SB_LUT_RGB, SB_NO_COLOR, StyleBlitError, check, lib
 
 __all__ = [
     "Params", "build_lut", "build_lut3", "exemplar_bytes", "prepare_exemplar", "stylize", "stylize_batch", "vote", "stylize_batch_host", "launch_count",
-    "version", "SB_JITTER_ZERO", "SB_NO_COLOR", "SB_LABEL", "SB_LUT_RGB", "StyleBlitError",
+    "version", "SB_JITTER_ZERO", "SB_NO_COLOR", "SB_LABEL", "SB_LUT_RGB", "SB_HOST_RGB", "StyleBlitError",
 ]
 
 
@@ -220,12 +220,14 @@ def stylize_batch_host(prm: Params, cs: torch.Tensor, gs: torch.Tensor, lut: tor
                        ct_host: torch.Tensor, coords_host: torch.Tensor | None = None, frame_seeds=None,
                        workspace: torch.Tensor | None = None, depth: int = 2, stream=None):
     """sb_stylize_batch_host: HOST gt [N,H,W,4] in, HOST ct [N,H,W,4] out (pinned memory for
-    full copy bandwidth); copies and compute overlap inside the library.  Blocks until done."""
+    full copy bandwidth); copies and compute overlap inside the library.  Blocks until done.
+    With prm.flags & SB_HOST_RGB the host frames are packed RGB: gt [N,H,W,3], ct [N,H,W,3]."""
+    ch = 3 if prm.flags & SB_HOST_RGB else 4
     for t, name in ((gt_host, "gt_host"), (ct_host, "ct_host")):
-        if t.is_cuda or t.dtype != torch.uint8 or not t.is_contiguous() or t.dim() != 4:
-            raise ValueError(f"{name} must be a contiguous host uint8 [N,H,W,4] tensor")
+        if t.is_cuda or t.dtype != torch.uint8 or not t.is_contiguous() or t.dim() != 4 or t.shape[-1] != ch:
+            raise ValueError(f"{name} must be a contiguous host uint8 [N,H,W,{ch}] tensor")
     n = int(gt_host.shape[0])
-    wt, ht = _img_wh(gt_host, "gt_host")
+    wt, ht = int(gt_host.shape[2]), int(gt_host.shape[1])
     ws, hs = _img_wh(gs, "gs")
     if workspace is None:
         workspace = host_workspace(wt, ht, prm.blend_radius, depth, device=cs.device)

@@ -18,6 +18,7 @@ SB_JITTER_ZERO = 0x1
 SB_NO_COLOR = 0x2
 SB_LABEL = 0x4
 SB_LUT_RGB = 0x8
+SB_HOST_RGB = 0x10
 SB_MAX_LEVELS = 12
 SB_MAX_RADIUS = 7
 

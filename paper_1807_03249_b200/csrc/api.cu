@@ -70,7 +70,7 @@ sb_status validate(const sb_params* prm, int32_t n_frames, const uint8_t* cs, co
         return fail(SB_EINVAL, "blend_radius r=%d outside [0,%d]", prm->blend_radius, SB_MAX_RADIUS);
     if (prm->guide_channels < 2 || prm->guide_channels > 4)
         return fail(SB_EINVAL, "guide_channels C=%d not in {2,3,4}", prm->guide_channels);
-    if (prm->flags & ~(SB_JITTER_ZERO | SB_NO_COLOR | SB_LABEL | SB_LUT_RGB))
+    if (prm->flags & ~(SB_JITTER_ZERO | SB_NO_COLOR | SB_LABEL | SB_LUT_RGB | SB_HOST_RGB))
         return fail(SB_EINVAL, "flags 0x%x has unknown bits", prm->flags);
     if ((prm->flags & SB_LABEL) && (prm->label_channel < 0 || prm->label_channel > 3))
         return fail(SB_EINVAL, "label_channel=%d outside [0,3]", prm->label_channel);
@@ -226,6 +226,8 @@ sb_status sb_stylize_batch(const sb_params* prm, int32_t n_frames, const uint32_
                            const uint8_t* gs, int32_t ws, int32_t hs, const uint32_t* lut, const uint8_t* gt,
                            int32_t wt, int32_t ht, uint8_t* ct, uint32_t* coords, uint8_t* level, void* stream) {
     g_launches = 0;
+    if (prm && (prm->flags & SB_HOST_RGB))
+        return fail(SB_EINVAL, "flags: SB_HOST_RGB applies to sb_stylize_batch_host only");
     Prepared p;
     sb_status s = validate(prm, n_frames, cs, gs, ws, hs, lut, gt, wt, ht, ct, coords, true, &p);
     if (s != SB_OK) return s;
@@ -272,7 +274,8 @@ static size_t host_seg_bytes(int32_t wt, int32_t ht) { return (((size_t)wt * (si
 size_t sb_host_workspace_bytes(int32_t wt, int32_t ht, int32_t blend_radius, int32_t depth) {
     if (wt < 1 || ht < 1 || depth < 1) return 0;
     (void)blend_radius;
-    return 3 * host_seg_bytes(wt, ht) * (size_t)depth;
+    // per slot: G_T, C_T, coords (RGBA / uint32) + packed-RGB staging in and out (SB_HOST_RGB)
+    return 5 * host_seg_bytes(wt, ht) * (size_t)depth;
 }
 
 sb_status sb_stylize_batch_host(const sb_params* prm, int32_t n_frames, const uint32_t* frame_seeds,
@@ -293,7 +296,15 @@ sb_status sb_stylize_batch_host(const sb_params* prm, int32_t n_frames, const ui
     if (wt < 1 || ht < 1) return fail(SB_EINVAL, "target (wt,ht): dimensions %dx%d", wt, ht);
     const size_t fpx = (size_t)wt * (size_t)ht;
     const size_t seg = host_seg_bytes(wt, ht);
-    auto slot_ptr = [&](int k, int part) { return static_cast<uint8_t*>(workspace) + ((size_t)k * 3 + part) * seg; };
+    auto slot_ptr = [&](int k, int part) { return static_cast<uint8_t*>(workspace) + ((size_t)k * 5 + part) * seg; };
+    const bool rgb = prm && (prm->flags & SB_HOST_RGB);
+    if (rgb) {
+        if (prm->guide_channels > 3) return fail(SB_EINVAL, "SB_HOST_RGB needs guide_channels <= 3");
+        if ((prm->flags & SB_LABEL) && prm->label_channel == 3)
+            return fail(SB_EINVAL, "SB_HOST_RGB: label_channel 3 is not carried by packed RGB frames");
+        if (wt % 4 != 0) return fail(SB_EUNSUPPORTED, "SB_HOST_RGB needs wt %% 4 == 0 (got %d)", wt);
+    }
+    const size_t hb = rgb ? 3 : 4;  // host bytes per pixel
     Prepared p;
     sb_status s = validate(prm, 1, cs, gs, ws, hs, lut, slot_ptr(0, 0), wt, ht, slot_ptr(0, 1),
                            reinterpret_cast<uint32_t*>(slot_ptr(0, 2)), true, &p);
@@ -327,10 +338,17 @@ sb_status sb_stylize_batch_host(const sb_params* prm, int32_t n_frames, const ui
         uint8_t* dct = slot_ptr(k, 1);
         uint32_t* dco = reinterpret_cast<uint32_t*>(slot_ptr(k, 2));
         if (i >= depth) cudaStreamWaitEvent(sH2D, outDone[k], 0);  // slot free again
-        e = cudaMemcpyAsync(dgt, gt_host + 4 * fpx * (size_t)i, 4 * fpx, cudaMemcpyHostToDevice, sH2D);
+        uint8_t* stage_in = slot_ptr(k, 3);
+        uint8_t* stage_out = slot_ptr(k, 4);
+        e = cudaMemcpyAsync(rgb ? stage_in : dgt, gt_host + hb * fpx * (size_t)i, hb * fpx, cudaMemcpyHostToDevice,
+                            sH2D);
         if (e != cudaSuccess) { st = cuda_fail(e, "H2D copy"); break; }
         cudaEventRecord(inReady[k], sH2D);
         cudaStreamWaitEvent(sCmp, inReady[k], 0);
+        if (rgb) {
+            e = sb::launch_unpack_rgb(stage_in, dgt, fpx, sCmp, &total_launches);
+            if (e != cudaSuccess) { st = cuda_fail(e, "unpack launch"); break; }
+        }
         Prepared pf = p;
         pf.s.gt = dgt;
         pf.s.ct = pf.s.ct ? dct : nullptr;
@@ -341,10 +359,15 @@ sb_status sb_stylize_batch_host(const sb_params* prm, int32_t n_frames, const ui
         total_launches += g_launches;
         g_launches = 0;
         if (st != SB_OK) break;
+        if (rgb && ct_host) {
+            e = sb::launch_pack_rgb(dct, stage_out, fpx, sCmp, &total_launches);
+            if (e != cudaSuccess) { st = cuda_fail(e, "pack launch"); break; }
+        }
         cudaEventRecord(cmpDone[k], sCmp);
         cudaStreamWaitEvent(sD2H, cmpDone[k], 0);
         if (ct_host) {
-            e = cudaMemcpyAsync(ct_host + 4 * fpx * (size_t)i, dct, 4 * fpx, cudaMemcpyDeviceToHost, sD2H);
+            e = cudaMemcpyAsync(ct_host + hb * fpx * (size_t)i, rgb ? stage_out : dct, hb * fpx,
+                                cudaMemcpyDeviceToHost, sD2H);
             if (e != cudaSuccess) { st = cuda_fail(e, "D2H copy"); break; }
         }
         if (coords_host) {

@@ -50,6 +50,8 @@ cudaError_t launch_build_lut(const uint8_t* gs, int ws, int hs, uint32_t* lut, v
                              cudaStream_t st, int* launches);
 cudaError_t launch_build_lut3(const uint8_t* gs, int ws, int hs, uint32_t* lut3, void* workspace,
                               cudaStream_t st, int* launches);
+cudaError_t launch_unpack_rgb(const uint8_t* rgb, uint8_t* rgba, size_t n_px, cudaStream_t st, int* launches);
+cudaError_t launch_pack_rgb(const uint8_t* rgba, uint8_t* rgb, size_t n_px, cudaStream_t st, int* launches);
 cudaError_t launch_prepare_exemplar(const uint8_t* cs, const uint8_t* gs, int ws, int hs, uint8_t* exemplar,
                                     cudaStream_t st, int* launches);
 cudaError_t launch_stylize_naive(const StylizeArgs& a, int n_frames, cudaStream_t st, int* launches);

@@ -144,6 +144,21 @@ def test_exemplar_copy_abi(lib):
     assert st == _lib.SB_EINVAL and "exemplar" in lib.sb_last_error().decode()
 
 
+def test_host_rgb_flag(lib):
+    p = _prm(flags=_lib.SB_HOST_RGB)
+    # device entry points refuse it
+    st = lib.sb_stylize(C.byref(p), FAKE, FAKE, 64, 64, FAKE, FAKE, 64, 64, FAKE, 0, 0, None)
+    assert st == _lib.SB_EINVAL and "SB_HOST_RGB" in lib.sb_last_error().decode()
+    ws = lib.sb_host_workspace_bytes(64, 64, 0, 2)
+    p4 = _prm(flags=_lib.SB_HOST_RGB, guide_channels=4)
+    st = lib.sb_stylize_batch_host(C.byref(p4), 1, None, FAKE, FAKE, 64, 64, FAKE, FAKE, 64, 64, FAKE, 0, FAKE, ws, 2,
+                                   None)
+    assert st == _lib.SB_EINVAL and "guide_channels" in lib.sb_last_error().decode()
+    st = lib.sb_stylize_batch_host(C.byref(p), 1, None, FAKE, FAKE, 64, 64, FAKE, FAKE, 62, 64, FAKE, 0, FAKE,
+                                   lib.sb_host_workspace_bytes(62, 64, 0, 2), 2, None)
+    assert st == _lib.SB_EUNSUPPORTED and "wt" in lib.sb_last_error().decode()
+
+
 def test_host_batch_invalid(lib):
     p = _prm()
     st = lib.sb_stylize_batch_host(C.byref(p), 1, None, FAKE, FAKE, 64, 64, FAKE, FAKE, 64, 64, FAKE, 0, FAKE, 16, 2,

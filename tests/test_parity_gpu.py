@@ -262,6 +262,14 @@ def test_host_pipeline_equals_device_batch():
         co_h = torch.empty(5, 288, 512, dtype=torch.int32).pin_memory()
         sb.stylize_batch_host(prm, cs, gs, lut, gt_h, ct_h, co_h, depth=2)
         assert torch.equal(ct_h, dct.cpu()) and torch.equal(co_h, dco.cpu())
+        # packed-RGB host frames (SB_HOST_RGB; guide byte 3 is not read with C = 3), with the
+        # strided exemplar copy: the same coordinates and the colours' channels 0..2
+        prgb = sb.Params(**{**prm.__dict__, "flags": sb.SB_HOST_RGB, "exemplar": sb.prepare_exemplar(cs, gs)})
+        g3 = frames[..., :3].contiguous().pin_memory()
+        c3 = torch.empty_like(g3).pin_memory()
+        co3 = torch.empty(5, 288, 512, dtype=torch.int32).pin_memory()
+        sb.stylize_batch_host(prgb, cs, gs, lut, g3, c3, co3, depth=3)
+        assert torch.equal(c3, dct.cpu()[..., :3]) and torch.equal(co3, dco.cpu())
 
 
 def test_naive_kernel_agrees(tmp_path):
