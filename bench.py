@@ -179,7 +179,7 @@ def run_ours(args):
     coords = torch.empty(B, HT, WT, dtype=torch.int32, device=dev)
     ct = torch.empty(B, HT, WT, 4, dtype=torch.uint8, device=dev)
     lut = torch.empty(65536, dtype=torch.int32, device=dev)
-    lut_ws = torch.empty(65536 * 4, dtype=torch.uint8, device=dev)
+    lut_ws = torch.empty(sb.lib().sb_lut_workspace_bytes(), dtype=torch.uint8, device=dev)
     ex = torch.empty(sb.exemplar_bytes(cs.shape[1], cs.shape[0]), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     p2p = strip and world > 1 and args.gather == "p2p"

@@ -110,7 +110,7 @@ typedef struct {
     const uint8_t* exemplar;
 } sb_params;
 
-/* Bytes of device workspace sb_build_lut needs (65536 x 4). */
+/* Bytes of device workspace sb_build_lut needs (65536 x 12: sites, then per-column nearest sites). */
 size_t sb_lut_workspace_bytes(void);
 
 /* Guide LUT: lut[k] = x | y<<16 of the source pixel u minimising

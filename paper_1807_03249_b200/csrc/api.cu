@@ -164,7 +164,7 @@ sb_status launch_frames(Prepared& p, int n_frames, const uint32_t* frame_seeds, 
 
 extern "C" {
 
-size_t sb_lut_workspace_bytes(void) { return 65536 * sizeof(uint32_t); }
+size_t sb_lut_workspace_bytes(void) { return 65536 * (sizeof(uint32_t) + 2 * sizeof(uint32_t)); }
 
 sb_status sb_build_lut(const uint8_t* gs, int32_t ws, int32_t hs, uint32_t* lut, void* workspace, void* stream) {
     g_launches = 0;

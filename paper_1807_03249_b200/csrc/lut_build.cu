@@ -7,13 +7,15 @@
 //
 //   1. sites:   site[g1][g0] = min row-major index of the source pixels with guide (g0,g1)
 //               (warp-deduplicated atomicMin; only the first pixel of a guide value can win).
-//   2. resolve: one CTA per key row k1.  Thread a finds, in guide column a, the site b
-//               minimising (k1-b)^2 (ties -> smaller pixel index: a site of column a with a
-//               larger (k1-b)^2 can never tie the total).  Then thread k0 takes the minimum
-//               over the 256 columns of (k0-a)^2 + f(a), ties -> smaller pixel index.
+//   2. columns: for every key row k1 and guide column a, the site b of column a minimising
+//               (k1-b)^2 (ties -> smaller pixel index: a site of column a with a larger
+//               (k1-b)^2 can never tie the total) -- the nearest occupied row above and below
+//               k1, from warp scans (one warp per column).
+//   3. resolve: one CTA per key row k1; thread k0 takes the minimum over the 256 columns of
+//               (k0-a)^2 + f(a), ties -> smaller pixel index.
 //
-// Work: ws*hs scatter + 2 x 256^3 compare-selects (~33 M), independent of the exemplar
-// size; the 256 KB site table stays in L2.
+// Work: ws*hs scatter + 256^2 column entries + 256^3 compare-selects (~17 M), independent of
+// the exemplar size; the 256 KB site table and the 512 KB column table stay in L2.
 #include "sb_device.cuh"
 
 namespace sb {
@@ -36,33 +38,98 @@ __global__ void __launch_bounds__(256) lut_sites_kernel(const uint32_t* __restri
     }
 }
 
-__global__ void __launch_bounds__(256) lut_resolve_kernel(const uint32_t* __restrict__ site, int ws,
+// pass 1, all rows at once: one warp per guide column a; lane j owns the 8 rows b = 8j..8j+7.
+// For every row k1 the nearest occupied site of column a: the last site at or above k1 and the
+// first at or below it (warp max / min scans), the closer one, ties -> smaller pixel index.
+// Output col[k1 * 256 + a] = (d, idx), d = (k1 - b)^2 (0xFFFFFFFF: empty column).
+__global__ void __launch_bounds__(256) lut_columns_kernel(const uint32_t* __restrict__ site,
+                                                          uint2* __restrict__ col) {
+    const int lane = threadIdx.x & 31;
+    const int a = blockIdx.x * 8 + (threadIdx.x >> 5);
+    uint32_t idx[8];
+    int last = -1, first = 256;  // last / first occupied row within this lane's 8 rows
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        idx[k] = __ldg(site + (8 * lane + k) * 256 + a);
+        if (idx[k] != 0xFFFFFFFFu) {
+            last = 8 * lane + k;
+            if (first == 256) first = 8 * lane + k;
+        }
+    }
+    // exclusive scans across lanes: last occupied row above this lane, first below it
+    int above = last, below = first;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xFFFFFFFFu, above, o);
+        const int dn = __shfl_down_sync(0xFFFFFFFFu, below, o);
+        if (lane >= o) above = max(above, u);
+        if (lane + o < 32) below = min(below, dn);
+    }
+    int prev = __shfl_up_sync(0xFFFFFFFFu, above, 1);   // last occupied row before this lane
+    int next = __shfl_down_sync(0xFFFFFFFFu, below, 1); // first occupied row after this lane
+    if (lane == 0) prev = -1;
+    if (lane == 31) next = 256;
+    // site pixel index of a row (only read for occupied rows)
+    auto idx_of = [&](int b) -> uint32_t {
+        const int owner = b >> 3;
+        uint32_t v = 0xFFFFFFFFu;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t t = __shfl_sync(0xFFFFFFFFu, idx[k], owner & 31);
+            if ((b & 7) == k) v = t;
+        }
+        return v;
+    };
+    // nearest occupied row at or above / at or below each of the lane's rows
+    int up[8], dnr[8];
+    int cur = prev;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        if (idx[k] != 0xFFFFFFFFu) cur = 8 * lane + k;
+        up[k] = cur;
+    }
+    cur = next;
+#pragma unroll
+    for (int k = 7; k >= 0; --k) {
+        if (idx[k] != 0xFFFFFFFFu) cur = 8 * lane + k;
+        dnr[k] = cur;
+    }
+    // the pixel indices of the rows up[k] / dnr[k] live in other lanes: fetch them with shuffles
+    // (every lane takes part in every shuffle, so the loops stay warp-uniform)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int k1 = 8 * lane + k;
+        const int bu = up[k], bd = dnr[k];
+        const uint32_t iu = idx_of(bu < 0 ? 0 : bu), id = idx_of(bd > 255 ? 0 : bd);
+        uint32_t d = 0xFFFFFFFFu, i = 0xFFFFFFFFu;
+        if (bu >= 0) { d = (uint32_t)((k1 - bu) * (k1 - bu)); i = iu; }
+        if (bd <= 255) {
+            const uint32_t dd = (uint32_t)((bd - k1) * (bd - k1));
+            if (dd < d || (dd == d && id < i)) { d = dd; i = id; }
+        }
+        col[k1 * 256 + a] = make_uint2(d, i);
+    }
+}
+
+// pass 2: one CTA per key row k1; thread k0 takes the minimum over the 256 columns of
+// (k0-a)^2 + f(a), ties -> smaller pixel index.
+__global__ void __launch_bounds__(256) lut_resolve_kernel(const uint2* __restrict__ col, int ws,
                                                           uint32_t* __restrict__ lut) {
     __shared__ uint32_t col_d[256];
     __shared__ uint32_t col_i[256];
     const int k1 = blockIdx.x;
-    const int a = threadIdx.x;
-    // pass 1: nearest site of column a to row k1 (1-D, tie -> smaller pixel index)
-    uint32_t bd = 0xFFFFFFFFu, bi = 0xFFFFFFFFu;
-#pragma unroll 8
-    for (int b = 0; b < 256; ++b) {
-        const uint32_t idx = __ldg(site + b * 256 + a);
-        const int dy = k1 - b;
-        const uint32_t d = (idx == 0xFFFFFFFFu) ? 0xFFFFFFFFu : (uint32_t)(dy * dy);
-        if (d < bd || (d == bd && idx < bi)) { bd = d; bi = idx; }
-    }
-    col_d[a] = bd;
-    col_i[a] = bi;
+    const uint2 c = __ldg(col + k1 * 256 + threadIdx.x);
+    col_d[threadIdx.x] = c.x;
+    col_i[threadIdx.x] = c.y;
     __syncthreads();
-    // pass 2: minimum over columns of (k0-a)^2 + f(a), tie -> smaller pixel index
     const int k0 = threadIdx.x;
     uint32_t best_d = 0xFFFFFFFFu, best_i = 0xFFFFFFFFu;
 #pragma unroll 8
-    for (int c = 0; c < 256; ++c) {
-        const uint32_t fd = col_d[c];
-        const int dx = k0 - c;
+    for (int cc = 0; cc < 256; ++cc) {
+        const uint32_t fd = col_d[cc];
+        const int dx = k0 - cc;
         const uint32_t d = (fd == 0xFFFFFFFFu) ? 0xFFFFFFFFu : fd + (uint32_t)(dx * dx);
-        const uint32_t fi = col_i[c];
+        const uint32_t fi = col_i[cc];
         if (d < best_d || (d == best_d && fi < best_i)) { best_d = d; best_i = fi; }
     }
     const uint32_t y = best_i / (uint32_t)ws, x = best_i - y * (uint32_t)ws;
@@ -77,8 +144,10 @@ cudaError_t launch_build_lut(const uint8_t* gs, int ws, int hs, uint32_t* lut, v
     int blocks = (n + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     lut_sites_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(gs), n, site);
-    lut_resolve_kernel<<<256, 256, 0, st>>>(site, ws, lut);
-    *launches += 3;
+    uint2* col = reinterpret_cast<uint2*>(site + 65536);  // 256 x 256 (d, idx) after the sites
+    lut_columns_kernel<<<32, 256, 0, st>>>(site, col);
+    lut_resolve_kernel<<<256, 256, 0, st>>>(col, ws, lut);
+    *launches += 4;
     return cudaPeekAtLastError();
 }
 

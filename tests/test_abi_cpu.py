@@ -48,7 +48,7 @@ def test_sm100a_cubin_present(lib):
 
 def test_version_and_workspace(lib):
     assert b"sm_100a" in lib.sb_version()
-    assert lib.sb_lut_workspace_bytes() == 65536 * 4
+    assert lib.sb_lut_workspace_bytes() == 65536 * 12
     assert lib.sb_lut3_workspace_bytes() == (1 << 24) * 8
     assert lib.sb_host_workspace_bytes(3840, 2160, 0, 2) >= 2 * 3 * 3840 * 2160 * 4
     assert lib.sb_host_workspace_bytes(0, 10, 0, 2) == 0
