@@ -287,8 +287,10 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteAr
                 const int yy = ry + R + dy;
                 const uint32_t b = (uint32_t)(x - R + 32);
                 const uint32_t bits = __funnelshift_r(hl[yy][b >> 5], hl[yy][(b >> 5) + 1], b & 31u);
-                const uint32_t m = ~bits & ((1u << (2 * R)) - 1u);  // at most one run end
-                const uint32_t c1 = m ? (uint32_t)__ffs(m) : W;      // length of run 1
+                // length of run 1 = position of the first run end + 1 (W if none): with t the
+                // link bits, t ^ (t + 1) has exactly c1 low bits set
+                const uint32_t t = bits & ((1u << (2 * R)) - 1u);
+                const uint32_t c1 = (uint32_t)__popc(t ^ (t + 1u));
                 const uint32_t h2 = c1 < W ? c1 : 0u;                // head of run 2 (or any)
                 const uint32_t* row = &sc[yy][OFF + x - R];
                 const uint32_t shy = (uint32_t)dy * wsl;

@@ -47,7 +47,9 @@ def _samples(rng, n, margin=0):
 def test_fullsize_blit(bench_batch):
     b = bench_batch
     cfg = b["cfg"]
-    prm = sb.Params(threshold=cfg["t"], levels=cfg["L"], guide_channels=cfg["C"], seed=cfg["seed"])
+    # the bench's launch configuration, with the strided exemplar copy
+    prm = sb.Params(threshold=cfg["t"], levels=cfg["L"], guide_channels=cfg["C"], seed=cfg["seed"],
+                    exemplar=sb.prepare_exemplar(b["cs"], b["gs"]))
     lut = sb.build_lut(b["gs"])
     ct, coords, _ = sb.stylize_batch(prm, b["cs"], b["gs"], lut, b["gt"], frame_seeds=b["seeds"], want_level=False)
     torch.cuda.synchronize()
@@ -66,11 +68,12 @@ def test_fullsize_blit(bench_batch):
 def test_fullsize_blend_r2(bench_batch):
     b = bench_batch
     cfg = b["cfg"]
+    ex = sb.prepare_exemplar(b["cs"], b["gs"])
     prm = sb.Params(threshold=cfg["t"], levels=cfg["L"], guide_channels=cfg["C"], seed=cfg["seed"],
-                    flags=sb.SB_NO_COLOR)
+                    flags=sb.SB_NO_COLOR, exemplar=ex)
     lut = sb.build_lut(b["gs"])
     _, coords, _ = sb.stylize_batch(prm, b["cs"], b["gs"], lut, b["gt"], frame_seeds=b["seeds"], want_level=False)
-    ct = sb.vote(coords, b["cs"], 2)
+    ct = sb.vote(coords, b["cs"], 2, exemplar=ex)
     torch.cuda.synchronize()
     rng = np.random.RandomState(2)
     for f in FRAMES[:2]:
@@ -92,7 +95,8 @@ def test_fullsize_blend_r2(bench_batch):
 def test_fullsize_lut_rgb(bench_batch):
     b = bench_batch
     cfg = b["cfg"]
-    prm = sb.Params(threshold=cfg["t"], levels=cfg["L"], guide_channels=cfg["C"], seed=cfg["seed"], lut_rgb=True)
+    prm = sb.Params(threshold=cfg["t"], levels=cfg["L"], guide_channels=cfg["C"], seed=cfg["seed"], lut_rgb=True,
+                    exemplar=sb.prepare_exemplar(b["cs"], b["gs"]))
     lut3 = sb.build_lut3(b["gs"])
     ct, coords, _ = sb.stylize_batch(prm, b["cs"], b["gs"], lut3, b["gt"], frame_seeds=b["seeds"], want_level=False)
     torch.cuda.synchronize()
