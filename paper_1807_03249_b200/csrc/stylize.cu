@@ -1,7 +1,8 @@
 // stylize.cu -- tiled Alg. 2 "ParallelStyleBlit" for sm_100a.
 //
-// One CTA = one 128 x 32 pixel tile of one frame (grid = tiles_x x tiles_y x frames), 256
-// threads; warp w owns tile rows 4w .. 4w+3 and a thread owns 4 consecutive pixels of each
+// One CTA = one 128 x 16 pixel tile of one frame (grid = tiles_x x tiles_y x frames), 128
+// threads, 8 CTAs per SM (small CTAs: a CTA waiting at its table-build barrier idles only 4
+// warps); warp w owns tile rows 4w .. 4w+3 and a thread owns 4 consecutive pixels of each
 // (uint4 I/O), i.e. a 4-aligned 4 x 4 pixel block.  Per tile and level l the seed cells that
 // any tile pixel can reach (its 3x3 neighbourhood) are materialised in
 // shared memory: the NearestSeed key words of the jittered seed s (SeedPoint, lines 354-358;
@@ -34,19 +35,19 @@ namespace sb {
 
 namespace {
 constexpr int TW = 128;           // tile width  (pixels)
-constexpr int TH = 32;            // tile height (pixels)
-constexpr int NT = 256;           // threads per CTA
+constexpr int TH = 16;            // tile height (pixels)
+constexpr int NT = 128;           // threads per CTA
 constexpr int TP = TW * TH;       // pixels per tile
 constexpr int NG = TW / 4;        // 4-pixel groups per row
 constexpr int NW = NT / 32;       // warps per CTA
 constexpr int RPW = TH / NW;      // rows per warp (RPW w .. RPW w + RPW-1)
 constexpr int WPX = TP / NW;      // pixels per warp
 // tables kept at once: levels {L, L-1, L-2} with h >= 4, i.e. at most levels 4, 3, 2
-// Tables are column-major with a fixed column stride CS = 13 cells (208 bytes = 52 words: 8
-// neighbouring columns start in 8 distinct even banks, so the 8-byte loads of lanes in
-// different columns do not conflict).  CS >= TH/4 + 4, the most cells a column of a level
-// with h = 4 spans.
-constexpr int CS = 13;
+// Tables are column-major with a fixed column stride CS = 9 slots (72 bytes = 18 words of the
+// 8-byte key table: neighbouring columns start in distinct banks).  CS >= TH/4 + 4, the most
+// cells a column of a level with h = 4 spans.
+constexpr int CS = 9;
+static_assert(CS >= TH / 4 + 4, "column stride must hold a column of the h = 4 level");
 __host__ __device__ constexpr int cells_of(int h) { return (TW / h + 3) * CS; }
 constexpr int MAXCELLS = cells_of(4) + cells_of(8) + cells_of(16);
 // table slots for a hierarchy of L levels: levels L, L-1, L-2 that have h >= 4
@@ -286,7 +287,7 @@ __device__ __forceinline__ uint32_t direct_candidate(const StylizeArgs& a, const
 // folds), LT = 0: a.L at run time.  PAD: the exemplar gathers index the strided copy
 // a.exemplar (sb_prepare_exemplar) with the packed coordinate itself.
 template <bool EXT, bool LVL, int LT, bool PAD>
-__global__ void __launch_bounds__(NT, 4) stylize_tiled_kernel(const __grid_constant__ StylizeArgs a) {
+__global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_constant__ StylizeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
     const int L = LT > 0 ? LT : a.L;
