@@ -13,7 +13,10 @@
  *                     extension of PAPER.md:423-433 ("randomization of seed points").
  *
  * plus sb_stylize_batch_host (the same batch with HOST frame buffers, streamed through
- * the device by a double-buffered copy/compute pipeline) and status helpers.
+ * the device by a double-buffered copy/compute pipeline), sb_vote (the vote alone),
+ * sb_build_lut3 (the exact three-channel guide search), sb_prepare_exemplar (an optional
+ * strided exemplar copy that makes packed source coordinates their own gather index) and
+ * status helpers.
  *
  * Conventions (all entry points)
  * ------------------------------
