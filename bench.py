@@ -441,7 +441,8 @@ def run_ours(args):
         "kernels": kernels,
         "roofline_issue": roof_issue,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                     "frac": round(ach / hbm, 4), "traffic": traffic, "peak_source": hbm_src,
+                     "frac": round(ach / hbm, 4), "frac_nominal_8tbs": round(ach / 8000.0, 4),
+                     "traffic": traffic, "peak_source": hbm_src,
                      "alg_bytes_per_launch": alg[dom], "alg_bytes_per_px": alg[dom] // px_step},
         "gpu_launches": main["launches"],
         "clocks": main["clocks"],
