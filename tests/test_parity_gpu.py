@@ -371,13 +371,15 @@ def test_weighted_and_segmentation_parity(case):
 # ------------------------------------------------------------------ CUDA graph capture
 def test_cuda_graph_capture_replay():
     """The ABI calls only enqueue work on the caller's stream (no allocation, no sync), so a
-    whole step (LUT + stylize + vote) can be captured into a CUDA graph and replayed: replays
+    whole step (LUT + strided exemplar copy + stylize + vote) can be captured into a CUDA graph and replayed: replays
     reproduce the eager result bit for bit, and follow new inputs written into the same buffers."""
     cfg = synth.CONFIGS[2]
     cs, gs = (t.to(DEV) for t in synth.exemplar(cfg))
     gt = synth.target(2).to(DEV).unsqueeze(0).repeat(3, 1, 1, 1).contiguous()
     gt[1] = torch.flip(gt[1], dims=[1])
-    prm = sb.Params(threshold=cfg["t"], levels=cfg["L"], blend_radius=2, guide_channels=cfg["C"], seed=cfg["seed"])
+    ex = torch.empty(sb.exemplar_bytes(gs.shape[1], gs.shape[0]), dtype=torch.uint8, device=DEV)
+    prm = sb.Params(threshold=cfg["t"], levels=cfg["L"], blend_radius=2, guide_channels=cfg["C"], seed=cfg["seed"],
+                    exemplar=ex)
     lut = torch.empty(65536, dtype=torch.int32, device=DEV)
     lws = torch.empty(sb.lib().sb_lut_workspace_bytes(), dtype=torch.uint8, device=DEV)
     ct = torch.empty_like(gt)
@@ -385,6 +387,7 @@ def test_cuda_graph_capture_replay():
 
     def step():
         sb.build_lut(gs, lut, lws)
+        sb.prepare_exemplar(cs, gs, ex)
         sb.stylize_batch(prm, cs, gs, lut, gt, ct=ct, coords=co, want_level=False)
 
     step()
