@@ -61,10 +61,17 @@ __host__ __device__ constexpr int table_cells(int L) {
 //   cq[slot] = (S2, X1)      the NearestSeed key terms (see KOFS below)
 //   cd[slot] = (Y1, delta)   delta = u* - q packed dy*65536 + dx
 struct Smem {
-    uint32_t coord[TP];           // result coords
+    uint32_t coord[TH * (TW + 4)];  // result coords, rows padded by 16 bytes (see cix)
     uint16_t wq[NW][WPX];         // per-warp pixel queue (compacted in place)
     uint16_t glist[NW][RPW * NG]; // per-warp list of groups with a rejected pixel
 };
+// coords slot of tile pixel (rx, ry) / of unpadded pixel index p = ry*TW + rx: rows are padded
+// by 4 words so that the 16-byte accesses of groups in different rows (the group passes) fall
+// into different banks
+constexpr int CROW = TW + 4;
+__device__ __forceinline__ int cix(int p) { return p + (p >> 7) * 4; }
+static_assert(TW == 128, "cix assumes 128-pixel rows");
+
 struct Cells {
     uint2* q;
     int2* d;
@@ -378,7 +385,7 @@ __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_const
                 // a rejected pixel's slot holds its G_T value until a finer level accepts it
                 // (the group passes and the pixel queue read it from there, not from global)
                 const uint4 g4 = gp[j - 1];
-                *reinterpret_cast<uint4*>(&sm.coord[ry * TW + rx0]) =
+                *reinterpret_cast<uint4*>(&sm.coord[ry * CROW + rx0]) =
                     make_uint4((acc & 1u) ? pcand[0] : g4.x, (acc & 2u) ? pcand[1] : g4.y,
                                (acc & 4u) ? pcand[2] : g4.z, (acc & 8u) ? pcand[3] : g4.w);
                 if (LVL) *reinterpret_cast<uint32_t*>(&lvl[ry * TW + rx0]) = 0x01010101u * (uint32_t)L;
@@ -419,7 +426,7 @@ __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_const
                     const uint32_t m = e >> 8;
                     const int pbase = ry * TW + grx0;
                     // the group's slots: coords of its accepted pixels, G_T of the rejected (m)
-                    uint4 cv = *reinterpret_cast<const uint4*>(&sm.coord[pbase]);
+                    uint4 cv = *reinterpret_cast<const uint4*>(&sm.coord[ry * CROW + grx0]);
                     uint32_t cand[4];
                     const uint32_t acc = group_eval<EXT, PAD>(T, a, gs, g, lp, x0, y0, grx0, ry, cv, m, cand);
                     // merge the newly accepted pixels: one 16-byte read-modify-write instead of
@@ -429,7 +436,7 @@ __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_const
                     cv.y = (take & 2u) ? cand[1] : cv.y;
                     cv.z = (take & 4u) ? cand[2] : cv.z;
                     cv.w = (take & 8u) ? cand[3] : cv.w;
-                    *reinterpret_cast<uint4*>(&sm.coord[pbase]) = cv;
+                    *reinterpret_cast<uint4*>(&sm.coord[ry * CROW + grx0]) = cv;
                     if (LVL) {
 #pragma unroll
                         for (int i = 0; i < 4; ++i)
@@ -480,7 +487,7 @@ __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_const
             if (!ok_of(j)) continue;
             for (int i = 0; i < 4; ++i) q[pos++] = (uint16_t)(row_of(j) * TW + rx0 + i);
             // the queue reads G_T from the pixel's slot
-            *reinterpret_cast<uint4*>(&sm.coord[row_of(j) * TW + rx0]) =
+            *reinterpret_cast<uint4*>(&sm.coord[row_of(j) * CROW + rx0]) =
                 *reinterpret_cast<const uint4*>(gtf + (uint32_t)((y0 + row_of(j)) * a.wt + x0 + rx0));
         }
         n = tot;
@@ -501,9 +508,9 @@ __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_const
                 idx = q[k];
                 const int rx = idx & (TW - 1), ry = idx / TW;
                 const uint32_t cand = direct_candidate(a, gtf, x0 + rx, y0 + ry, l, c_l);
-                const uint32_t gp = sm.coord[idx];  // G_T while the pixel is rejected
+                const uint32_t gp = sm.coord[cix(idx)];  // G_T while the pixel is rejected
                 if (accept<EXT, PAD>(a, gs, gp, cand)) {
-                    sm.coord[idx] = cand;
+                    sm.coord[cix(idx)] = cand;
                     if (LVL) lvl[idx] = (uint8_t)l;
                 } else {
                     rej = true;
@@ -521,7 +528,7 @@ __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_const
     if (l == 0) {
         for (int k = lane; k < n; k += 32) {
             const int idx = q[k];
-            sm.coord[idx] = __ldg(a.lut + (sm.coord[idx] & a.key_mask));  // the slot holds G_T
+            sm.coord[cix(idx)] = __ldg(a.lut + (sm.coord[cix(idx)] & a.key_mask));  // the slot holds G_T
             if (LVL) lvl[idx] = 0;
         }
     }
@@ -536,7 +543,7 @@ __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_const
         if (!ok_of(j)) continue;
         const int ry = row_of(j);
         const int64_t o = fpx * frame + (int64_t)((y0 + ry) * wt + (uint32_t)(x0 + rx0));
-        const uint4 cv = *reinterpret_cast<const uint4*>(&sm.coord[ry * TW + rx0]);
+        const uint4 cv = *reinterpret_cast<const uint4*>(&sm.coord[ry * CROW + rx0]);
         if (a.coords) st_cs_u4(a.coords + o, cv);
         if (a.level) st_cs_u32(a.level + o, *reinterpret_cast<const uint32_t*>(&lvl[ry * TW + rx0]));
         if (a.ct) {
