@@ -469,7 +469,7 @@ def test_exemplar_copy_batch_and_strips(L):
     assert torch.equal(ct2, ct[0])
 
 
-@pytest.mark.parametrize("r", [1, 2, 3])
+@pytest.mark.parametrize("r", [1, 2, 3, 4, 5, 6, 7])
 def test_vote_exemplar_copy(r):
     """sb_vote with the strided exemplar copy equals sb_vote without it and the oracle, on a
     coordinate field with chunk seams, frame borders and sources at the exemplar border."""
