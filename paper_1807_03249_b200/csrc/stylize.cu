@@ -72,6 +72,8 @@ constexpr int CROW = TW + 4;
 __device__ __forceinline__ int cix(int p) { return p + (p >> 7) * 4; }
 static_assert(TW == 128, "cix assumes 128-pixel rows");
 
+static_assert(sizeof(Smem) % 16 == 0, "the cell tables after Smem need 16-byte alignment");
+
 struct Cells {
     uint2* q;
     int2* d;
