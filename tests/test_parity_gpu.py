@@ -357,8 +357,9 @@ def test_weighted_and_segmentation_parity(case):
     lut_d = sb.build_lut(gsd)
     lut = oracle_lut(gs.numpy())
     o = oracle.stylize(oracle.Params(seed=0x5EED, **okw), cs.numpy(), gs.numpy(), lut, gt.numpy(), nthreads=NTH)
-    for r in (0, 2):
-        ct, co, lv = sb.stylize(sb.Params(blend_radius=r, seed=0x5EED, **kw), csd, gsd, lut_d, gtd)
+    ex = sb.prepare_exemplar(csd, gsd)  # ignored by the weighted/label kernel, used by the vote
+    for r, exm in ((0, None), (2, None), (0, ex), (2, ex)):
+        ct, co, lv = sb.stylize(sb.Params(blend_radius=r, seed=0x5EED, exemplar=exm, **kw), csd, gsd, lut_d, gtd)
         assert (u32(co) == o[1]).all() and (lv.cpu().numpy() == o[2]).all()
         want = o[0] if r == 0 else oracle.vote(o[1], cs.numpy(), r, nthreads=NTH)
         assert (ct.cpu().numpy() == want).all()
