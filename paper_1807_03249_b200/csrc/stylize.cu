@@ -295,7 +295,7 @@ __device__ __forceinline__ uint32_t direct_candidate(const StylizeArgs& a, const
 // LT > 0: the hierarchy depth as a compile-time constant (the common depths; all level geometry
 // folds), LT = 0: a.L at run time.  PAD: the exemplar gathers index the strided copy
 // a.exemplar (sb_prepare_exemplar) with the packed coordinate itself.
-template <bool EXT, bool LVL, int LT, bool PAD>
+template <bool EXT, bool LVL, int LT, bool PAD, bool NOCT = false>
 __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_constant__ StylizeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_const
         const uint4 cv = *reinterpret_cast<const uint4*>(&sm.coord[ry * CROW + rx0]);
         if (a.coords) st_cs_u4(a.coords + o, cv);
         if (a.level) st_cs_u32(a.level + o, *reinterpret_cast<const uint32_t*>(&lvl[ry * TW + rx0]));
-        if (a.ct) {
+        if (!NOCT && a.ct) {
             uint4 col;
             // packed x | y<<16 -> pixel index y*ws + x (PAD: the packed value itself)
             auto idx = [&](uint32_t c) { return PAD ? c : (c >> 16) * ws + (c & 0xFFFFu); };
@@ -574,7 +574,11 @@ cudaError_t launch_stylize_tiled(const StylizeArgs& a, int n_frames, cudaStream_
              : a.L == 3 ? (pad ? stylize_tiled_kernel<false, true, 3, true> : stylize_tiled_kernel<false, true, 3, false>)
                         : stylize_tiled_kernel<false, true, 0, false>;
     } else {
-        kern = a.L == 5 ? (pad ? stylize_tiled_kernel<false, false, 5, true> : stylize_tiled_kernel<false, false, 5, false>)
+        // NOCT: coordinates only (the blend path: the vote makes the colours)
+        const bool noct = a.ct == nullptr;
+        kern = a.L == 5 ? (pad ? (noct ? stylize_tiled_kernel<false, false, 5, true, true>
+                                       : stylize_tiled_kernel<false, false, 5, true>)
+                               : stylize_tiled_kernel<false, false, 5, false>)
              : a.L == 4 ? (pad ? stylize_tiled_kernel<false, false, 4, true> : stylize_tiled_kernel<false, false, 4, false>)
              : a.L == 3 ? (pad ? stylize_tiled_kernel<false, false, 3, true> : stylize_tiled_kernel<false, false, 3, false>)
                         : stylize_tiled_kernel<false, false, 0, false>;
