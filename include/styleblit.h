@@ -28,7 +28,10 @@
  *  - The LUT has 65536 uint32 entries indexed by key = G[0] | G[1] << 8 (the first two
  *    guide channels, the paper's "two values").
  *  - Unless a name says _host, every pointer is a DEVICE pointer.  The caller owns every
- *    buffer; the library allocates nothing persistent and keeps no state between calls.
+ *    buffer; the library allocates no device memory and keeps no state between calls except
+ *    host-side caches that never change results: per device, the SM count and the kernels'
+ *    shared-memory attributes; per thread and device, the 3 streams and 25 events of the
+ *    sb_stylize_batch_host pipeline (created on its first call, drained before it returns).
  *  - Work is enqueued on `stream` (a cudaStream_t passed as void*; NULL = legacy default
  *    stream) and the call returns after launch (asynchronous), except
  *    sb_stylize_batch_host, which returns when its results are in host memory.
@@ -139,8 +142,13 @@ sb_status sb_build_lut3(const uint8_t* gs, int32_t ws, int32_t hs, uint32_t* lut
                         void* workspace, void* stream);
 
 /* Bytes of the strided exemplar copy for a ws x hs exemplar: G_S and C_S, each hs rows of
- * 2^16 pixels (row stride 256 KiB), i.e. 2 * hs * 2^18 bytes (256 MiB for hs = 512).  Only
- * ws pixels of a row are written and read; the rest is never touched.  ws <= 32767.        */
+ * 2^16 pixels (row stride 256 KiB), i.e. 2 * hs * 2^18 bytes (256 MiB for hs = 512, 1 GiB
+ * for hs = 2048).  Only ws pixels of a row are written and read (2 * ws * hs * 4 bytes, the
+ * exemplar's own size, are ever touched), but the whole range must be allocated.  Capped at
+ * hs <= SB_EXEMPLAR_MAX_HS (2 GiB): returns 0 above it (and for ws > 32767), and such
+ * exemplars are used directly (sb_params.exemplar = NULL; identical results, a few percent
+ * slower).                                                                                 */
+#define SB_EXEMPLAR_MAX_HS 4096
 size_t sb_exemplar_bytes(int32_t ws, int32_t hs);
 
 /* The strided exemplar copy used through sb_params.exemplar: exemplar[0 .. hs*2^18) holds
@@ -148,7 +156,8 @@ size_t sb_exemplar_bytes(int32_t ws, int32_t hs);
  * so a packed source coordinate x | y<<16 is its own pixel index (the two
  * exemplar gathers of Alg. 2).  Rebuild it whenever cs or gs change (like the LUT).
  *   cs, gs     device, ws*hs*4: style exemplar C_S and source guide G_S
- *   exemplar   device, sb_exemplar_bytes(ws, hs) bytes, 16-byte aligned, output           */
+ *   exemplar   device, sb_exemplar_bytes(ws, hs) bytes, 16-byte aligned, output
+ * SB_EUNSUPPORTED for hs > SB_EXEMPLAR_MAX_HS.                                            */
 sb_status sb_prepare_exemplar(const uint8_t* cs, const uint8_t* gs, int32_t ws, int32_t hs,
                               uint8_t* exemplar, void* stream);
 

@@ -123,6 +123,9 @@ def prepare_exemplar(cs: torch.Tensor, gs: torch.Tensor, out: torch.Tensor | Non
     ws, hs = _img_wh(gs, "gs")
     if _img_wh(cs, "cs") != (ws, hs):
         raise ValueError("cs and gs must have the same size")
+    if exemplar_bytes(ws, hs) == 0:
+        raise ValueError(f"no strided exemplar copy for a {ws}x{hs} exemplar (hs > SB_EXEMPLAR_MAX_HS); "
+                         "use Params(exemplar=None)")
     if out is None:
         out = torch.empty(exemplar_bytes(ws, hs), dtype=torch.uint8, device=gs.device)
     _dev(out, "out", torch.uint8, (1,))
@@ -138,15 +141,53 @@ def _check_lut(prm: Params, lut: torch.Tensor) -> None:
         raise ValueError(f"lut has {lut.numel()} entries; {'lut_rgb' if prm.lut_rgb else '2-channel'} needs {want}")
 
 
+def _check_out(t: torch.Tensor, name: str, shape: tuple[int, ...], dtype: torch.dtype, device) -> None:
+    """A caller-supplied output must match exactly: the ABI takes raw pointers, so a short
+    buffer would be overrun by the kernels."""
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if t.device != torch.device(device):
+        raise ValueError(f"{name} is on {t.device}, the inputs on {device}")
+    if t.dtype != dtype or tuple(t.shape) != tuple(shape) or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous {dtype} tensor of shape {tuple(shape)}, "
+                         f"got {t.dtype} {tuple(t.shape)}")
+
+
 def _outputs(prm: Params, shape_px: tuple[int, ...], device, ct, coords, level, want_level: bool):
     no_color = bool(prm.flags & SB_NO_COLOR)
     if ct is None and not no_color:
         ct = torch.empty(*shape_px, 4, dtype=torch.uint8, device=device)
+    elif ct is not None:
+        _check_out(ct, "ct", (*shape_px, 4), torch.uint8, device)
     if coords is None:
         coords = torch.empty(*shape_px, dtype=torch.int32, device=device)
+    else:
+        _check_out(coords, "coords", shape_px, torch.int32, device)
     if level is None and want_level:
         level = torch.empty(*shape_px, dtype=torch.uint8, device=device)
+    elif level is not None:
+        _check_out(level, "level", shape_px, torch.uint8, device)
     return ct, coords, level
+
+
+def _check_exemplar(ex: torch.Tensor | None, ws: int, hs: int, device) -> None:
+    if ex is None:
+        return
+    need = exemplar_bytes(ws, hs)
+    if need == 0:
+        raise ValueError(f"no strided exemplar copy for a {ws}x{hs} exemplar (hs > SB_EXEMPLAR_MAX_HS); pass None")
+    if ex.device != torch.device(device) or ex.dtype != torch.uint8 or ex.numel() < need:
+        raise ValueError(f"exemplar must be a uint8 tensor of >= {need} bytes on {device} "
+                         f"(prepare_exemplar(cs, gs)), got {ex.dtype} {ex.numel()} bytes on {ex.device}")
+
+
+def _seeds(frame_seeds, n: int):
+    if frame_seeds is None:
+        return None
+    seeds = [int(s) & 0xFFFFFFFF for s in frame_seeds]
+    if len(seeds) != n:
+        raise ValueError(f"frame_seeds has {len(seeds)} entries for {n} frames")
+    return (C.c_uint32 * n)(*seeds)
 
 
 def stylize(prm: Params, cs: torch.Tensor, gs: torch.Tensor, lut: torch.Tensor, gt: torch.Tensor,
@@ -176,10 +217,12 @@ def stylize_batch(prm: Params, cs: torch.Tensor, gs: torch.Tensor, lut: torch.Te
     n = int(gt.shape[0])
     wt, ht = _img_wh(gt, "gt")
     ct, coords, level = _outputs(prm, (n, ht, wt), gt.device, ct, coords, level, want_level)
+    _check_exemplar(prm.exemplar, ws, hs, gt.device)
+    for t, name in ((cs, "cs"), (gs, "gs"), (lut, "lut")):
+        if t.device != gt.device:
+            raise ValueError(f"{name} is on {t.device}, gt on {gt.device}")
     ptr = lambda t, name, dt, nd: 0 if t is None else _dev(t, name, dt, nd)  # noqa: E731
-    seeds = None
-    if frame_seeds is not None:
-        seeds = (C.c_uint32 * n)(*[int(s) & 0xFFFFFFFF for s in frame_seeds])
+    seeds = _seeds(frame_seeds, n)
     p = prm.c()
     check(lib().sb_stylize_batch(C.byref(p), n, seeds, cs.data_ptr(), gs.data_ptr(), ws, hs, lut.data_ptr(),
                                  gt.data_ptr(), wt, ht, ptr(ct, "ct", torch.uint8, (4,)),
@@ -205,7 +248,10 @@ def vote(coords: torch.Tensor, cs: torch.Tensor, r: int, ct: torch.Tensor | None
         ct = torch.empty(n, ht, wt, 4, dtype=torch.uint8, device=co.device)
     elif squeeze:
         ct = ct.unsqueeze(0)
-    _dev(ct, "ct", torch.uint8, (4,))
+    _check_out(ct, "ct", (n, ht, wt, 4), torch.uint8, co.device)
+    if cs.device != co.device:
+        raise ValueError(f"cs is on {cs.device}, coords on {co.device}")
+    _check_exemplar(exemplar, ws, hs, co.device)
     ex = None if exemplar is None else _dev(exemplar, "exemplar", torch.uint8, (1,))
     check(lib().sb_vote(co.data_ptr(), n, wt, ht, cs.data_ptr(), ws, hs, int(r), ct.data_ptr(), int(row_begin),
                         int(row_end), ex, _stream(stream)))
@@ -226,14 +272,22 @@ def stylize_batch_host(prm: Params, cs: torch.Tensor, gs: torch.Tensor, lut: tor
     for t, name in ((gt_host, "gt_host"), (ct_host, "ct_host")):
         if t.is_cuda or t.dtype != torch.uint8 or not t.is_contiguous() or t.dim() != 4 or t.shape[-1] != ch:
             raise ValueError(f"{name} must be a contiguous host uint8 [N,H,W,{ch}] tensor")
+    if tuple(ct_host.shape) != tuple(gt_host.shape):
+        raise ValueError(f"ct_host shape {tuple(ct_host.shape)} != gt_host shape {tuple(gt_host.shape)}")
     n = int(gt_host.shape[0])
     wt, ht = int(gt_host.shape[2]), int(gt_host.shape[1])
+    if coords_host is not None:
+        if (coords_host.is_cuda or coords_host.dtype != torch.int32 or not coords_host.is_contiguous()
+                or tuple(coords_host.shape) != (n, ht, wt)):
+            raise ValueError(f"coords_host must be a contiguous host int32 tensor of shape {(n, ht, wt)}")
     ws, hs = _img_wh(gs, "gs")
     if workspace is None:
         workspace = host_workspace(wt, ht, prm.blend_radius, depth, device=cs.device)
-    seeds = None
-    if frame_seeds is not None:
-        seeds = (C.c_uint32 * n)(*[int(s) & 0xFFFFFFFF for s in frame_seeds])
+    need = int(lib().sb_host_workspace_bytes(wt, ht, prm.blend_radius, depth))
+    if workspace.device != cs.device or workspace.numel() * workspace.element_size() < need:
+        raise ValueError(f"workspace must hold >= {need} bytes on {cs.device}")
+    _check_exemplar(prm.exemplar, ws, hs, cs.device)
+    seeds = _seeds(frame_seeds, n)
     _check_lut(prm, lut)
     p = prm.c()
     check(lib().sb_stylize_batch_host(C.byref(p), n, seeds, _dev(cs, "cs", torch.uint8, (3,)),

@@ -160,6 +160,52 @@ sb_status launch_frames(Prepared& p, int n_frames, const uint32_t* frame_seeds, 
     return SB_OK;
 }
 
+// The host pipeline's streams and events: created on first use per (thread, device) and
+// reused by every later sb_stylize_batch_host call on that thread and device (one pipeline
+// runs at a time per thread, and every call drains it before returning).
+struct Pipeline {
+    cudaStream_t h2d = nullptr, cmp = nullptr, d2h = nullptr;
+    cudaEvent_t start = nullptr;
+    cudaEvent_t in_ready[8] = {}, cmp_done[8] = {}, out_done[8] = {};
+};
+
+sb_status pipeline(Pipeline** out) {
+    thread_local Pipeline cache[16];
+    thread_local bool ready[16] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (dev < 0 || dev >= 16) return fail(SB_EUNSUPPORTED, "device index %d >= 16", dev);
+    Pipeline& p = cache[dev];
+    if (!ready[dev]) {
+        Pipeline q;
+        auto undo = [&](cudaError_t err, const char* what) {
+            for (cudaStream_t s : {q.h2d, q.cmp, q.d2h})
+                if (s) cudaStreamDestroy(s);
+            for (int k = 0; k < 8; ++k)
+                for (cudaEvent_t ev : {q.in_ready[k], q.cmp_done[k], q.out_done[k]})
+                    if (ev) cudaEventDestroy(ev);
+            if (q.start) cudaEventDestroy(q.start);
+            return cuda_fail(err, what);
+        };
+        if ((e = cudaStreamCreateWithFlags(&q.h2d, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&q.cmp, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&q.d2h, cudaStreamNonBlocking)) != cudaSuccess)
+            return undo(e, "pipeline stream creation");
+        if ((e = cudaEventCreateWithFlags(&q.start, cudaEventDisableTiming)) != cudaSuccess)
+            return undo(e, "pipeline event creation");
+        for (int k = 0; k < 8; ++k)
+            if ((e = cudaEventCreateWithFlags(&q.in_ready[k], cudaEventDisableTiming)) != cudaSuccess ||
+                (e = cudaEventCreateWithFlags(&q.cmp_done[k], cudaEventDisableTiming)) != cudaSuccess ||
+                (e = cudaEventCreateWithFlags(&q.out_done[k], cudaEventDisableTiming)) != cudaSuccess)
+                return undo(e, "pipeline event creation");
+        p = q;
+        ready[dev] = true;
+    }
+    *out = &p;
+    return SB_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -181,7 +227,7 @@ sb_status sb_build_lut(const uint8_t* gs, int32_t ws, int32_t hs, uint32_t* lut,
 }
 
 size_t sb_exemplar_bytes(int32_t ws, int32_t hs) {
-    if (ws < 1 || hs < 1 || ws > 32767 || hs > 32767) return 0;
+    if (ws < 1 || hs < 1 || ws > 32767 || hs > SB_EXEMPLAR_MAX_HS) return 0;
     return (size_t)2 * (size_t)hs * ((size_t)1 << 18);
 }
 
@@ -193,6 +239,9 @@ sb_status sb_prepare_exemplar(const uint8_t* cs, const uint8_t* gs, int32_t ws, 
     if (!gs) return fail(SB_EINVAL, "gs (source guide G_S) is NULL");
     if (!exemplar) return fail(SB_EINVAL, "exemplar is NULL (need sb_exemplar_bytes(ws, hs) bytes)");
     if ((s = check_dims("source (ws,hs)", ws, hs)) != SB_OK) return s;
+    if (hs > SB_EXEMPLAR_MAX_HS)
+        return fail(SB_EUNSUPPORTED, "hs=%d > SB_EXEMPLAR_MAX_HS=%d: the strided copy would need %zu MiB; pass "
+                    "exemplar = NULL instead", hs, SB_EXEMPLAR_MAX_HS, ((size_t)hs << 19) >> 20);
     if (!aligned16(cs) || !aligned16(gs) || !aligned16(exemplar))
         return fail(SB_EINVAL, "cs/gs/exemplar must be 16-byte aligned");
     cudaError_t e = sb::launch_prepare_exemplar(cs, gs, ws, hs, exemplar, (cudaStream_t)stream, &g_launches);
@@ -254,7 +303,6 @@ sb_status sb_vote(const uint32_t* coords, int32_t n_frames, int32_t wt, int32_t 
                     ht);
     if (!aligned16(coords) || !aligned16(cs) || !aligned16(ct) || (exemplar && !aligned16(exemplar)))
         return fail(SB_EINVAL, "coords/cs/ct/exemplar must be 16-byte aligned");
-    if (wt % 4 != 0) return fail(SB_EUNSUPPORTED, "sb_vote needs wt %% 4 == 0 (got %d); use sb_stylize", wt);
     const int64_t fpx = (int64_t)wt * ht;
     for (int f0 = 0; f0 < n_frames; f0 += 65535) {
         const int nf = (n_frames - f0) < 65535 ? (n_frames - f0) : 65535;
@@ -284,6 +332,7 @@ sb_status sb_stylize_batch_host(const sb_params* prm, int32_t n_frames, const ui
                                 uint32_t* coords_host, void* workspace, size_t workspace_bytes, int32_t depth,
                                 void* stream) {
     g_launches = 0;
+    if (n_frames < 0) return fail(SB_EINVAL, "n_frames=%d < 0", n_frames);
     if (depth < 1 || depth > 8) return fail(SB_EINVAL, "depth=%d outside [1,8]", depth);
     if (!workspace) return fail(SB_EINVAL, "workspace is NULL");
     if (!gt_host) return fail(SB_EINVAL, "gt_host is NULL");
@@ -306,30 +355,22 @@ sb_status sb_stylize_batch_host(const sb_params* prm, int32_t n_frames, const ui
     }
     const size_t hb = rgb ? 3 : 4;  // host bytes per pixel
     Prepared p;
-    sb_status s = validate(prm, 1, cs, gs, ws, hs, lut, slot_ptr(0, 0), wt, ht, slot_ptr(0, 1),
+    sb_status s = validate(prm, n_frames, cs, gs, ws, hs, lut, slot_ptr(0, 0), wt, ht, slot_ptr(0, 1),
                            reinterpret_cast<uint32_t*>(slot_ptr(0, 2)), true, &p);
     if (s != SB_OK) return s;
     if (prm->row_begin != 0 || prm->row_end != 0) return fail(SB_EUNSUPPORTED, "host batches are whole frames");
     if (n_frames == 0) return SB_OK;
 
     cudaStream_t user = (cudaStream_t)stream;
-    cudaStream_t sH2D, sCmp, sD2H;
+    Pipeline* pl = nullptr;
+    if ((s = pipeline(&pl)) != SB_OK) return s;
+    cudaStream_t sH2D = pl->h2d, sCmp = pl->cmp, sD2H = pl->d2h;
+    cudaEvent_t start = pl->start, *inReady = pl->in_ready, *cmpDone = pl->cmp_done, *outDone = pl->out_done;
     cudaError_t e;
-    if ((e = cudaStreamCreateWithFlags(&sH2D, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
-    cudaStreamCreateWithFlags(&sCmp, cudaStreamNonBlocking);
-    cudaStreamCreateWithFlags(&sD2H, cudaStreamNonBlocking);
-    cudaEvent_t start, *inReady = new cudaEvent_t[depth], *cmpDone = new cudaEvent_t[depth],
-                       *outDone = new cudaEvent_t[depth];
-    cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
-    for (int k = 0; k < depth; ++k) {
-        cudaEventCreateWithFlags(&inReady[k], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&cmpDone[k], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&outDone[k], cudaEventDisableTiming);
-    }
     // everything is ordered after the work already queued on the caller's stream
-    cudaEventRecord(start, user);
-    cudaStreamWaitEvent(sH2D, start, 0);
-    cudaStreamWaitEvent(sCmp, start, 0);
+    if ((e = cudaEventRecord(start, user)) != cudaSuccess || (e = cudaStreamWaitEvent(sH2D, start, 0)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(sCmp, start, 0)) != cudaSuccess)
+        return cuda_fail(e, "pipeline ordering");
     int total_launches = 0;
     sb_status st = SB_OK;
     for (int i = 0; i < n_frames && st == SB_OK; ++i) {
@@ -337,14 +378,20 @@ sb_status sb_stylize_batch_host(const sb_params* prm, int32_t n_frames, const ui
         uint8_t* dgt = slot_ptr(k, 0);
         uint8_t* dct = slot_ptr(k, 1);
         uint32_t* dco = reinterpret_cast<uint32_t*>(slot_ptr(k, 2));
-        if (i >= depth) cudaStreamWaitEvent(sH2D, outDone[k], 0);  // slot free again
+        if (i >= depth && (e = cudaStreamWaitEvent(sH2D, outDone[k], 0)) != cudaSuccess) {  // slot free again
+            st = cuda_fail(e, "pipeline ordering");
+            break;
+        }
         uint8_t* stage_in = slot_ptr(k, 3);
         uint8_t* stage_out = slot_ptr(k, 4);
         e = cudaMemcpyAsync(rgb ? stage_in : dgt, gt_host + hb * fpx * (size_t)i, hb * fpx, cudaMemcpyHostToDevice,
                             sH2D);
         if (e != cudaSuccess) { st = cuda_fail(e, "H2D copy"); break; }
-        cudaEventRecord(inReady[k], sH2D);
-        cudaStreamWaitEvent(sCmp, inReady[k], 0);
+        if ((e = cudaEventRecord(inReady[k], sH2D)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(sCmp, inReady[k], 0)) != cudaSuccess) {
+            st = cuda_fail(e, "pipeline ordering");
+            break;
+        }
         if (rgb) {
             e = sb::launch_unpack_rgb(stage_in, dgt, fpx, sCmp, &total_launches);
             if (e != cudaSuccess) { st = cuda_fail(e, "unpack launch"); break; }
@@ -363,8 +410,11 @@ sb_status sb_stylize_batch_host(const sb_params* prm, int32_t n_frames, const ui
             e = sb::launch_pack_rgb(dct, stage_out, fpx, sCmp, &total_launches);
             if (e != cudaSuccess) { st = cuda_fail(e, "pack launch"); break; }
         }
-        cudaEventRecord(cmpDone[k], sCmp);
-        cudaStreamWaitEvent(sD2H, cmpDone[k], 0);
+        if ((e = cudaEventRecord(cmpDone[k], sCmp)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(sD2H, cmpDone[k], 0)) != cudaSuccess) {
+            st = cuda_fail(e, "pipeline ordering");
+            break;
+        }
         if (ct_host) {
             e = cudaMemcpyAsync(ct_host + hb * fpx * (size_t)i, rgb ? stage_out : dct, hb * fpx,
                                 cudaMemcpyDeviceToHost, sD2H);
@@ -374,25 +424,18 @@ sb_status sb_stylize_batch_host(const sb_params* prm, int32_t n_frames, const ui
             e = cudaMemcpyAsync(coords_host + fpx * (size_t)i, dco, 4 * fpx, cudaMemcpyDeviceToHost, sD2H);
             if (e != cudaSuccess) { st = cuda_fail(e, "D2H copy"); break; }
         }
-        cudaEventRecord(outDone[k], sD2H);
+        if ((e = cudaEventRecord(outDone[k], sD2H)) != cudaSuccess) {
+            st = cuda_fail(e, "pipeline ordering");
+            break;
+        }
     }
+    // drain all three streams (also after an error, so the cached pipeline is idle again)
     e = cudaStreamSynchronize(sD2H);
     cudaError_t e2 = cudaStreamSynchronize(sCmp);
-    cudaStreamSynchronize(sH2D);
+    cudaError_t e3 = cudaStreamSynchronize(sH2D);
     if (st == SB_OK && e != cudaSuccess) st = cuda_fail(e, "pipeline sync");
     if (st == SB_OK && e2 != cudaSuccess) st = cuda_fail(e2, "pipeline sync");
-    for (int k = 0; k < depth; ++k) {
-        cudaEventDestroy(inReady[k]);
-        cudaEventDestroy(cmpDone[k]);
-        cudaEventDestroy(outDone[k]);
-    }
-    delete[] inReady;
-    delete[] cmpDone;
-    delete[] outDone;
-    cudaEventDestroy(start);
-    cudaStreamDestroy(sH2D);
-    cudaStreamDestroy(sCmp);
-    cudaStreamDestroy(sD2H);
+    if (st == SB_OK && e3 != cudaSuccess) st = cuda_fail(e3, "pipeline sync");
     g_launches = total_launches;
     return st;
 }

@@ -14,7 +14,7 @@
 // winner has a smaller or equal index among the line's minimisers), so the tie rule holds.
 // Each pass is a dense 256-candidate scan per entry: 2^32 compare-selects per pass, on a
 // 128 MiB (distance, index) workspace, in place (a CTA owns whole lines).
-#include "sb_device.cuh"
+#include "sb_kernels.cuh"
 
 namespace sb {
 
@@ -103,11 +103,11 @@ cudaError_t launch_build_lut3(const uint8_t* gs, int ws, int hs, uint32_t* lut3,
     lut3_init_kernel<<<N / 4 / 256, 256, 0, st>>>(site);
     const int n = ws * hs;
     int blocks = (n + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > sm_count() * 16) blocks = sm_count() * 16;
     lut3_sites_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(gs), n, site);
     lut3_seed_kernel<<<N / 256, 256, 0, st>>>(site, d);
     const int smem = 256 * LCP * (int)sizeof(uint2);
-    cudaError_t e = cudaFuncSetAttribute(lut3_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = ensure_smem(reinterpret_cast<const void*>(lut3_pass_kernel), smem);
     if (e != cudaSuccess) return e;
     const dim3 grid(256 / LC, 256);
     lut3_pass_kernel<<<grid, NT3, smem, st>>>(d, 1, 256, 65536);      // along k0, columns k1, rest k2

@@ -16,7 +16,7 @@
 //
 // Work: ws*hs scatter + 256^2 column entries + 256^3 compare-selects (~17 M), independent of
 // the exemplar size; the 256 KB site table and the 512 KB column table stay in L2.
-#include "sb_device.cuh"
+#include "sb_kernels.cuh"
 
 namespace sb {
 
@@ -142,7 +142,7 @@ cudaError_t launch_build_lut(const uint8_t* gs, int ws, int hs, uint32_t* lut, v
     lut_init_kernel<<<65536 / 4 / 256, 256, 0, st>>>(site);
     const int n = ws * hs;
     int blocks = (n + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > sm_count() * 16) blocks = sm_count() * 16;
     lut_sites_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(gs), n, site);
     uint2* col = reinterpret_cast<uint2*>(site + 65536);  // 256 x 256 (d, idx) after the sites
     lut_columns_kernel<<<32, 256, 0, st>>>(site, col);

@@ -46,6 +46,11 @@ struct VoteArgs {
     int row_begin, row_end;  // rows written
 };
 
+// launch_util.cu: per-device cached SM count and one-time kernel attributes
+int sm_count();
+cudaError_t ensure_smem(const void* kern, int bytes);
+cudaError_t ensure_carveout(const void* kern, int pct);
+
 cudaError_t launch_build_lut(const uint8_t* gs, int ws, int hs, uint32_t* lut, void* workspace,
                              cudaStream_t st, int* launches);
 cudaError_t launch_build_lut3(const uint8_t* gs, int ws, int hs, uint32_t* lut3, void* workspace,
@@ -57,5 +62,6 @@ cudaError_t launch_prepare_exemplar(const uint8_t* cs, const uint8_t* gs, int ws
 cudaError_t launch_stylize_naive(const StylizeArgs& a, int n_frames, cudaStream_t st, int* launches);
 cudaError_t launch_stylize_tiled(const StylizeArgs& a, int n_frames, cudaStream_t st, int* launches);
 cudaError_t launch_vote(const VoteArgs& a, int n_frames, cudaStream_t st, int* launches);
+cudaError_t launch_vote_peel(const VoteArgs& a, int n_frames, cudaStream_t st, int* launches);
 
 }  // namespace sb

@@ -240,8 +240,9 @@ __device__ __forceinline__ uint32_t group_eval(const Cells& T, const StylizeArgs
     const uint32_t gpv[4] = {gp4.x, gp4.y, gp4.z, gp4.w};
     const uint32_t p0 = ((uint32_t)(y0 + ry) << 16) | (uint32_t)(x0 + rx0);
     uint32_t acc = 0;
-    // only the pixels in m (still rejected) look up their winner and gather: the others issue
-    // no shared or global request
+    // every pixel of the group looks up its winner and gathers (the caller keeps only the
+    // still-rejected ones, m & acc): predicating the look-ups per pixel measured slower
+    //
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         {
@@ -583,13 +584,13 @@ cudaError_t launch_stylize_tiled(const StylizeArgs& a, int n_frames, cudaStream_
              : a.L == 3 ? (pad ? stylize_tiled_kernel<false, false, 3, true> : stylize_tiled_kernel<false, false, 3, false>)
                         : stylize_tiled_kernel<false, false, 0, false>;
     }
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), (int)smem);
     if (e != cudaSuccess) return e;
     static const int carve = [] {
         const char* ev = getenv("SB_STYLIZE_CARVEOUT");
         return ev ? atoi(ev) : -1;
     }();
-    if (carve >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+    if ((e = ensure_carveout(reinterpret_cast<const void*>(kern), carve)) != cudaSuccess) return e;
     dim3 grid((unsigned)((a.wt + TW - 1) / TW), (unsigned)((a.row_end - (a.row_begin & ~3) + TH - 1) / TH),
               (unsigned)n_frames);
     kern<<<grid, NT, smem, st>>>(a);

@@ -30,6 +30,7 @@
 // packed sum src(q) + (p-q) never carries between fields and any position left of / above
 // the source wraps to a field >= 0xFFF0, which the bounds test rejects).
 #include <cstdlib>
+#include <cstring>
 
 #include "sb_kernels.cuh"
 
@@ -394,12 +395,17 @@ static int vote_carveout() {
 template <int R>
 static void launch_r(const VoteArgs& a, dim3 grid, cudaStream_t st) {
     auto kern = a.cs_pad ? vote_kernel<R, true> : vote_kernel<R, false>;
-    if (vote_carveout() >= 0)
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, vote_carveout());
+    ensure_carveout(reinterpret_cast<const void*>(kern), vote_carveout());  // a preference: failure is harmless
     kern<<<grid, NT, 0, st>>>(a);
 }
 
 cudaError_t launch_vote(const VoteArgs& a, int n_frames, cudaStream_t st, int* launches) {
+    // SB_VOTE=peel: the peel vote of vote_peel.cu for r = 1, 2 (A/B; measured slower)
+    static const bool peel = [] {
+        const char* e = getenv("SB_VOTE");
+        return e && strcmp(e, "peel") == 0;
+    }();
+    if ((a.r == 1 || a.r == 2) && peel) return launch_vote_peel(a, n_frames, st, launches);
     const int tiles = ((a.wt + TW - 1) / TW) * ((a.row_end - a.row_begin + TH - 1) / TH);
     dim3 grid((unsigned)tiles, (unsigned)n_frames);
     switch (a.r) {

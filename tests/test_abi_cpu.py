@@ -192,3 +192,36 @@ def test_product_does_not_import_oracle():
         if fn.endswith((".c", ".h", ".py")):
             txt = open(os.path.join(ROOT, "oracle", fn)).read()
             assert "import paper_1807_03249_b200" not in txt and "styleblit.h\"" not in txt
+
+
+def test_host_batch_negative_frames_and_exemplar_cap(lib):
+    p = _prm()
+    st = lib.sb_stylize_batch_host(C.byref(p), -1, None, FAKE, FAKE, 64, 64, FAKE, FAKE, 64, 64, FAKE, 0, FAKE,
+                                   lib.sb_host_workspace_bytes(64, 64, 0, 2), 2, None)
+    assert st == _lib.SB_EINVAL and "n_frames" in lib.sb_last_error().decode()
+    assert lib.sb_exemplar_bytes(512, 512) == 2 * 512 * (1 << 18)
+    assert lib.sb_exemplar_bytes(512, 4096) == 2 * 4096 * (1 << 18)
+    assert lib.sb_exemplar_bytes(512, 4097) == 0
+    st = lib.sb_prepare_exemplar(FAKE, FAKE, 64, 5000, FAKE, None)
+    assert st == _lib.SB_EUNSUPPORTED and "SB_EXEMPLAR_MAX_HS" in lib.sb_last_error().decode()
+
+
+def test_binding_output_and_seed_validation():
+    """The binding checks caller-supplied outputs (shape, dtype, device) and frame_seeds
+    before any raw pointer reaches the ABI (host-side logic, no GPU needed)."""
+    import torch
+
+    t = torch.zeros(2, 8, 8, dtype=torch.int32)
+    sb._check_out(t, "coords", (2, 8, 8), torch.int32, "cpu")
+    with pytest.raises(ValueError, match="shape"):
+        sb._check_out(t, "coords", (2, 8, 9), torch.int32, "cpu")
+    with pytest.raises(ValueError, match="shape"):
+        sb._check_out(t, "coords", (2, 8, 8), torch.uint8, "cpu")
+    with pytest.raises(ValueError, match="on"):
+        sb._check_out(t, "coords", (2, 8, 8), torch.int32, "meta")
+    assert sb._seeds(None, 3) is None
+    assert list(sb._seeds([1, 2, 3], 3)) == [1, 2, 3]
+    with pytest.raises(ValueError, match="frame_seeds"):
+        sb._seeds([1, 2], 3)
+    with pytest.raises(ValueError, match="frame_seeds"):
+        sb._seeds([1, 2, 3, 4], 3)

@@ -493,3 +493,37 @@ def test_vote_exemplar_copy(r):
     torch.cuda.synchronize()
     assert torch.equal(a, b)
     assert (b.cpu().numpy() == oracle.vote(co, cs.numpy(), r, nthreads=NTH)).all()
+
+
+@pytest.mark.parametrize("r", [1, 2])
+@pytest.mark.parametrize("chunk", [1, 2, 3, 5, 8, 32])
+def test_vote_peel_distinct_offsets(r, chunk):
+    """The peel vote (r = 1, 2; vote_peel.cu) against the oracle on fields whose 4x4-block
+    unions hold from one to (4+2r)^2 distinct offsets: chunk x chunk squares copying random
+    source blocks, sources kept >= r from the exemplar border so most tiles take the fast
+    path (chunk = 1: every position its own offset, the position-by-position leftovers after
+    KMAX peels); a frame border and a ragged width exercise the border tiles."""
+    rng = np.random.RandomState(100 * r + chunk)
+    ws, hs = 200, 180
+    cs = torch.from_numpy(rng.randint(0, 256, (hs, ws, 4)).astype(np.uint8))
+    gs = torch.zeros((hs, ws, 4), dtype=torch.uint8)
+    csd, gsd = cs.to(DEV), gs.to(DEV)
+    ex = sb.prepare_exemplar(csd, gsd)
+    for wt, ht in ((384, 48), (261, 37)):
+        yy, xx = np.mgrid[0:ht, 0:wt]
+        nby, nbx = ht // chunk + 1, wt // chunk + 1
+        ox = rng.randint(r, ws - chunk - r, (nby, nbx))
+        oy = rng.randint(r, hs - chunk - r, (nby, nbx))
+        sx = xx % chunk + ox[yy // chunk, xx // chunk]
+        sy = yy % chunk + oy[yy // chunk, xx // chunk]
+        co = (sx | (sy << 16)).astype(np.uint32)
+        cod = torch.from_numpy(co.view(np.int32)).to(DEV)
+        want = oracle.vote(co, cs.numpy(), r, nthreads=NTH)
+        for exm in (None, ex):
+            got = sb.vote(cod, csd, r, exemplar=exm)
+            torch.cuda.synchronize()
+            g = got.cpu().numpy()
+            if not (g == want).all():
+                bad = np.argwhere((g != want).any(-1))
+                raise AssertionError(f"{wt}x{ht} exemplar={exm is not None}: {len(bad)} pixels differ, "
+                                     f"first {bad[:4].tolist()}")
