@@ -59,6 +59,10 @@ def parse():
     ap.add_argument("--lut-rgb-steps", type=int, default=10,
                     help="timed steps of the exact 3-channel guide-search run (SB_LUT_RGB, 0: skip)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config sections (BASELINE configs 1, 2, 4, single-frame 4K latency, "
+                         "ragged width) and their oracle timings")
+    ap.add_argument("--config-steps", type=int, default=10, help="timed steps of each per-config section")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--json-out", default=None)
@@ -138,6 +142,198 @@ def peaks():
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------- per-config sections
+def _levels(torch, sb, prm_kw, cs, gs, lut, gt1, L):
+    """Level histogram of one frame (which level accepted each pixel) and the mean
+    number of levels a pixel visits; untimed."""
+    lv = torch.empty(gt1.shape[0], gt1.shape[1], dtype=torch.uint8, device=gt1.device)
+    sb.stylize(sb.Params(**prm_kw), cs, gs, lut, gt1, level=lv)
+    hist = torch.bincount(lv.flatten().long(), minlength=L + 1).double()
+    frac = (hist / hist.sum()).tolist()
+    visited = sum(f * (L - l + 1 if l >= 1 else L) for l, f in enumerate(frac))
+    return {"accepted_at_level": {str(l): round(frac[l], 4) for l in range(L, -1, -1)},
+            "mean_levels_visited": round(visited, 3)}
+
+
+def gpu_section(torch, sb, synth, dev, stream, hbm, cid, frames, rad, steps, warmup, wt=None, ht=None):
+    """One BASELINE config on the GPU: a batch of `frames` frames per step, the step being
+    sb_build_lut + sb_prepare_exemplar + sb_stylize_batch (+ sb_vote for rad > 0) as in the
+    headline; CUDA events on the launching stream around every call; value = frames x pixels /
+    step time.  wt/ht override the config's target size (the ragged-width row)."""
+    cfg = synth.CONFIGS[cid]
+    wt, ht = wt or cfg["wt"], ht or cfg["ht"]
+    cs, gs = [t.to(dev) for t in synth.exemplar(cfg, device=dev)]
+    if (wt, ht) == (cfg["wt"], cfg["ht"]):
+        firsts = [synth.target(cid, i, device=dev) for i in range(min(frames, 4 if cid in (1, 3, 5) else 1))]
+    else:
+        firsts = [synth.heightfield_normals(wt, ht, seed=5, frame=i, device=dev) for i in range(min(frames, 4))]
+    gt = torch.empty(frames, ht, wt, 4, dtype=torch.uint8, device=dev)
+    for i in range(frames):
+        gt[i] = firsts[i % len(firsts)]
+    seeds = [(cfg["seed"] + i) & 0xFFFFFFFF for i in range(frames)]
+    lut = torch.empty(65536, dtype=torch.int32, device=dev)
+    lut_ws = torch.empty(sb.lib().sb_lut_workspace_bytes(), dtype=torch.uint8, device=dev)
+    ex = torch.empty(sb.exemplar_bytes(cfg["ws"], cfg["hs"]), dtype=torch.uint8, device=dev)
+    coords = torch.empty(frames, ht, wt, dtype=torch.int32, device=dev)
+    ct = torch.empty(frames, ht, wt, 4, dtype=torch.uint8, device=dev)
+    prm = sb.Params(threshold=cfg["t"], levels=cfg["L"], guide_channels=cfg["C"], seed=cfg["seed"],
+                    flags=sb.SB_NO_COLOR if rad > 0 else 0, exemplar=ex)
+    names = ("lut", "exemplar", "stylize", "vote")
+    ev = {k: [] for k in names}
+    nl = [0]
+
+    def step(rec):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(5)] if rec else None
+        if rec:
+            e[0].record(stream)
+        sb.build_lut(gs, lut, lut_ws)
+        n = sb.launch_count()
+        if rec:
+            e[1].record(stream)
+        sb.prepare_exemplar(cs, gs, ex)
+        n += sb.launch_count()
+        if rec:
+            e[2].record(stream)
+        sb.stylize_batch(prm, cs, gs, lut, gt, frame_seeds=seeds, ct=None if rad > 0 else ct, coords=coords,
+                         want_level=False)
+        n += sb.launch_count()
+        if rec:
+            e[3].record(stream)
+        if rad > 0:
+            sb.vote(coords, cs, rad, ct=ct, exemplar=ex)
+            n += sb.launch_count()
+        if rec:
+            e[4].record(stream)
+            for k, (a, b) in zip(names, ((0, 1), (1, 2), (2, 3), (3, 4))):
+                ev[k].append((e[a], e[b]))
+            nl[0] += n
+
+    for _ in range(warmup):
+        step(False)
+    torch.cuda.synchronize(dev)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        step(True)
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = t0.elapsed_time(t1) / steps
+    px = frames * wt * ht
+    kt = {k: statistics.mean(a.elapsed_time(b) for a, b in v) for k, v in ev.items()}
+    alg = {"stylize": (8 if rad > 0 else 12) * px}
+    if rad > 0:
+        alg["vote"] = 8 * px
+    kernels = {k: {"ms_per_launch": round(kt[k], 4), "share": round(kt[k] / ms, 4)} for k in names if k != "vote" or rad}
+    dom = max(alg, key=lambda k: kt[k])
+    ach = alg[dom] / (kt[dom] * 1e-3) / 1e9
+    prm_l = dict(threshold=cfg["t"], levels=cfg["L"], guide_channels=cfg["C"], seed=cfg["seed"])
+    out = {"value": round(px / (ms * 1e-3) / 1e6, 1), "unit": "MP/s", "ms_per_step": round(ms, 4),
+           "frames_per_step": frames, "frame": f"{wt}x{ht}", "exemplar": f"{cfg['ws']}x{cfg['hs']}",
+           "L": cfg["L"], "t": cfg["t"], "C": cfg["C"], "blend_radius": rad,
+           "kernels": kernels, "gpu_launches": nl[0],
+           "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                        "frac": round(ach / hbm, 4), "alg_bytes_per_px": alg[dom] // px},
+           "levels": _levels(torch, sb, prm_l, cs, gs, lut, gt[0], cfg["L"])}
+    del gt, coords, ct, ex
+    return out
+
+
+def single_frame_latency(torch, sb, synth, dev, reps=200):
+    """One 4K frame (config 3) at a time, the paper's per-frame regime: the
+    per-frame calls captured once in a CUDA graph and replayed back to back (no launch
+    overhead); LUT and exemplar copy built once before (per exemplar, not per frame)."""
+    cfg = synth.CONFIGS[3]
+    cs, gs = [t.to(dev) for t in synth.exemplar(cfg, device=dev)]
+    gt = synth.target(3, 0, device=dev)
+    lut = sb.build_lut(gs)
+    ex = sb.prepare_exemplar(cs, gs)
+    coords = torch.empty(gt.shape[0], gt.shape[1], dtype=torch.int32, device=dev)
+    ct = torch.empty_like(gt)
+    out = {}
+    for rad in (0, 2):
+        prm = sb.Params(threshold=cfg["t"], levels=cfg["L"], guide_channels=cfg["C"], seed=cfg["seed"],
+                        blend_radius=rad, exemplar=ex)
+        s = torch.cuda.Stream(dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                sb.stylize(prm, cs, gs, lut, gt, ct=ct, coords=coords, want_level=False)
+        torch.cuda.current_stream(dev).wait_stream(s)
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            sb.stylize(prm, cs, gs, lut, gt, ct=ct, coords=coords, want_level=False)
+        for _ in range(10):
+            g.replay()
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            g.replay()
+        b.record()
+        torch.cuda.synchronize(dev)
+        ms = a.elapsed_time(b) / reps
+        out[f"r{rad}"] = {"ms_per_frame": round(ms, 4), "fps": round(1000.0 / ms, 1),
+                          "MPps": round(gt.shape[0] * gt.shape[1] / (ms * 1e-3) / 1e6, 1)}
+        del g
+    out["note"] = ("one 3840x2160 frame per CUDA-graph replay, replays back to back; r0 = stylize + blit, "
+                   "r2 = stylize + vote; LUT and exemplar copy built once per exemplar")
+    return out
+
+
+def oracle_section(cid, rad, frames_1t, frames_nt, nth):
+    """The CPU oracle (as it stands) on the same config: LUT built first (timed apart, excluded),
+    then stylize (+ vote) per frame at 1 thread and at nth threads."""
+    import oracle
+    import synth
+
+    cfg = synth.CONFIGS[cid]
+    cs, gs = [t.numpy() for t in synth.exemplar(cfg)]
+    gts = [synth.target(cid, i).numpy() for i in range(max(frames_1t, frames_nt) if cid in (1, 3, 5) else 1)]
+    t0 = time.perf_counter()
+    lut = oracle.build_lut(gs, nthreads=nth)
+    t_lut = time.perf_counter() - t0
+
+    def run(n, th):
+        t = time.perf_counter()
+        for i in range(n):
+            prm = oracle.Params(t=cfg["t"], L=cfg["L"], C=cfg["C"], seed=(cfg["seed"] + i) & 0xFFFFFFFF)
+            _, co, _ = oracle.stylize(prm, cs, gs, lut, gts[i % len(gts)], nthreads=th)
+            if rad > 0:
+                oracle.vote(co, cs, rad, nthreads=th)
+        return time.perf_counter() - t
+
+    px = cfg["wt"] * cfg["ht"]
+    d1, dn = run(frames_1t, 1), run(frames_nt, nth)
+    return {"value_1thread": round(frames_1t * px / d1 / 1e6, 3), "value_nthreads": round(frames_nt * px / dn / 1e6, 3),
+            "unit": "MP/s", "threads": nth, "kind": "oracle", "lut_build_s": round(t_lut, 2),
+            "sample": f"{frames_1t} frame(s) at 1 thread ({d1:.2f} s), {frames_nt} frame(s) at {nth} threads "
+                      f"({dn:.2f} s); stylize{' + vote r=%d' % rad if rad else ' (blit)'}; LUT build "
+                      f"({nth} threads) excluded"}
+
+
+def config_sections(args, torch, sb, synth, dev, stream, hbm, with_oracle):
+    """BASELINE.json configs other than the headline, each with its own value, roofline, level
+    histogram and the oracle timed beside it; plus the single-frame 4K latency and a ragged
+    width row.  Not part of the headline value."""
+    nth = os.cpu_count() or 1
+    st, wu = args.config_steps, 3
+    secs = {}
+    plan = [("cfg1_64px_normal_L3", 1, 4096, 0, (64, 4)),
+            ("cfg2_1MP_objects_L5_blend_r2", 2, 64, 2, (1, 1)),
+            ("cfg4_1MP_uvwarp_displacement_L5_blend_r2", 4, 64, 2, (1, 1))]
+    for name, cid, frames, rad, (f1, fn) in plan:
+        sec = gpu_section(torch, sb, synth, dev, stream, hbm, cid, frames, rad, st, wu)
+        if with_oracle:
+            sec["oracle"] = oracle_section(cid, rad, f1, fn, nth)
+        secs[name] = sec
+    secs["single_frame_4k"] = single_frame_latency(torch, sb, synth, dev)
+    rag = gpu_section(torch, sb, synth, dev, stream, hbm, 5, args.frames, 0, st, wu, wt=3838, ht=2160)
+    rag["note"] = "cfg5 workload at a width not divisible by 4 (3838): the tiled kernel's per-pixel row I/O"
+    secs["ragged_3838x2160"] = rag
+    return secs
 
 
 # ----------------------------------------------------------------------------------- ours
@@ -413,6 +609,14 @@ def run_ours(args):
         if cfg["C"] <= 3:
             e2e_rgb = run_e2e(True)
 
+    configs = None
+    if not args.no_configs and not strip:
+        del gt, coords, ct  # the sections allocate their own batches
+        configs = config_sections(args, torch, sb, synth, dev, stream, hbm,
+                                  with_oracle=(rank == 0 and world == 1 and not args.no_cpu_baseline))
+        if "ragged_3838x2160" in configs:
+            configs["ragged_3838x2160"]["vs_3840"] = round(configs["ragged_3838x2160"]["value"] / value, 4)
+
     # ---- parity spot check of this run's outputs (sampled pixels of frame 0 vs oracle) is in tests/.
     out = {
         "metric": "stylized megapixels/s (4K UHD frames/s) per B200 and 8-GPU; % HBM roofline",
@@ -451,41 +655,20 @@ def run_ours(args):
         "blend_r2": blend,
         "lut_rgb": lut_rgb,
         "levels": levels,
+        "configs": configs,
     }
     return out, rank, world
 
 
 # ----------------------------------------------------------------------------------- oracle
-def oracle_sample(n_frames: int, r: int, nthreads: int):
-    """The oracle (as it stands) on n 4K frames of the same workload: LUT, stylize, vote."""
-    import numpy as np
-
-    import oracle
-    import synth
-
-    cfg = synth.CONFIGS[CFG_ID]
-    cs, gs = [t.numpy() for t in synth.exemplar(cfg)]
-    frames = [synth.heightfield_normals(WT, HT, seed=5, frame=i).numpy() for i in range(n_frames)]
-    t0 = time.perf_counter()
-    lut = oracle.build_lut(gs, nthreads=nthreads)
-    t1 = time.perf_counter()
-    for i, f in enumerate(frames):
-        prm = oracle.Params(t=cfg["t"], L=cfg["L"], C=cfg["C"], seed=(cfg["seed"] + i) & 0xFFFFFFFF)
-        _, coords, _ = oracle.stylize(prm, cs, gs, lut, f, nthreads=nthreads)
-        if r > 0:
-            oracle.vote(coords, cs, r, nthreads=nthreads)
-    t2 = time.perf_counter()
-    return t1 - t0, t2 - t1, lut, cs, gs, frames, np
-
-
 def cpu_baseline(args):
-    n = 4
+    """The oracle on the headline workload: LUT built first (excluded, reported apart), then
+    stylize (+ vote) on 4 frames at all host threads and on 1 frame at 1 thread."""
     nth = os.cpu_count() or 1
-    t_lut, t_frames, *_ = oracle_sample(n, args.blend_radius, nth)
-    tot = t_lut + t_frames
-    return {"value": round(n * WT * HT / tot / 1e6, 3), "unit": "MP/s", "cores": nth, "kind": "oracle",
-            "sample": f"LUT build + {n} 4K frames (stylize{" + vote r=" + str(args.blend_radius) if args.blend_radius else ", blit colours"}) of the cfg5 workload on "
-                      f"{nth} host threads; {tot:.1f} s (LUT {t_lut:.1f} s)"}
+    sec = oracle_section(CFG_ID, args.blend_radius, 1, 4, nth)
+    return {"value": sec["value_nthreads"], "unit": "MP/s", "cores": nth, "kind": "oracle",
+            "value_1thread": sec["value_1thread"], "lut_build_s": sec["lut_build_s"],
+            "sample": "cfg5 4K frames: " + sec["sample"]}
 
 
 def run_reference(args):

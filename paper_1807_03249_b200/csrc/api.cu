@@ -37,15 +37,16 @@ sb_status check_dims(const char* name, int32_t w, int32_t h) {
     return SB_OK;
 }
 
-// Which stylize kernel: the tiled kernel needs wt % 4 == 0 (uint4 pixel groups per row) and
-// L <= 9 (its tabled NearestSeed keys 1024 d + code fit 32 bits for h <= 2^9, stylize.cu);
-// SB_KERNEL=naive selects the one-thread-per-pixel kernel (for A/B measurement).
+// Which stylize kernel: the tiled kernel (any width; ragged widths take its per-pixel row I/O
+// instantiation) needs L <= 9 (its tabled NearestSeed keys 1024 d + code fit 32 bits for
+// h <= 2^9, stylize.cu); SB_KERNEL=naive selects the one-thread-per-pixel kernel (A/B).
 bool use_naive(int32_t wt, int32_t L) {
     static const int forced = [] {
         const char* e = getenv("SB_KERNEL");
         return (e && strcmp(e, "naive") == 0) ? 1 : 0;
     }();
-    return forced || (wt % 4) != 0 || L > 9;
+    (void)wt;
+    return forced || L > 9;
 }
 
 struct Prepared {

@@ -296,7 +296,10 @@ __device__ __forceinline__ uint32_t direct_candidate(const StylizeArgs& a, const
 // LT > 0: the hierarchy depth as a compile-time constant (the common depths; all level geometry
 // folds), LT = 0: a.L at run time.  PAD: the exemplar gathers index the strided copy
 // a.exemplar (sb_prepare_exemplar) with the packed coordinate itself.
-template <bool EXT, bool LVL, int LT, bool PAD, bool NOCT = false>
+// RAG: a ragged width (wt % 4 != 0): rows are not 16-byte aligned and the last group of a row
+// has 1..3 pixels, so G_T is read and the outputs are written pixel by pixel there (pixels past
+// the row end are computed on G_T = 0 and never written).
+template <bool EXT, bool LVL, int LT, bool PAD, bool NOCT = false, bool RAG = false>
 __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_constant__ StylizeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -321,7 +324,8 @@ __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_const
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt_mask = (1u << lane) - 1u;
     const int rx0 = lane * 4;               // this thread's 4-pixel group column
-    const bool colok = x0 + rx0 < a.wt;     // wt % 4 == 0: a group is all in or all out
+    const bool colok = x0 + rx0 < a.wt;     // the group has a pixel inside the row
+    const int nin = min(4, a.wt - (x0 + rx0));  // its pixels inside the row (4 unless RAG)
     const int rows_here = min(TH, a.row_end - y0);
     const int row_lo = a.row_begin - y0;  // > 0 only in the first tile row of an unaligned range
     // tile row of this warp's j-th row, and whether its group exists
@@ -330,11 +334,15 @@ __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_const
 
     // The thread's 4 G_T rows (the HBM stream, consumed at level L) are issued first: their
     // latency overlaps the table build and its barrier.
+    // G_T of the group in row j: one 16-byte load, or (RAG) up to 4 scalar loads
+    auto load_gt = [&](int j) {
+        const uint32_t* p = gtf + (uint32_t)((y0 + row_of(j)) * a.wt + x0 + rx0);
+        if (!RAG) return *reinterpret_cast<const uint4*>(p);
+        return make_uint4(__ldg(p), nin > 1 ? __ldg(p + 1) : 0u, nin > 2 ? __ldg(p + 2) : 0u, nin > 3 ? __ldg(p + 3) : 0u);
+    };
     uint4 gp[RPW];
 #pragma unroll
-    for (int j = 0; j < RPW; ++j)
-        gp[j] = (L >= 2 && ok_of(j)) ? *reinterpret_cast<const uint4*>(gtf + (uint32_t)((y0 + row_of(j)) * a.wt + x0 + rx0))
-                                     : make_uint4(0u, 0u, 0u, 0u);
+    for (int j = 0; j < RPW; ++j) gp[j] = (L >= 2 && ok_of(j)) ? load_gt(j) : make_uint4(0u, 0u, 0u, 0u);
 
     // ---- tables of the levels among L, L-1, L-2 with h >= 4: the only CTA barrier ----
     const bool t0 = L >= 2, t1 = L - 1 >= 2, t2 = L - 2 >= 2;
@@ -483,15 +491,14 @@ __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_const
     } else {
         // L == 1: every valid pixel starts in the pixel queue
         int mine = 0;
-        for (int j = 0; j < RPW; ++j) mine += ok_of(j) ? 4 : 0;
+        for (int j = 0; j < RPW; ++j) mine += ok_of(j) ? nin : 0;
         int tot;
         int pos = warp_excl_scan(mine, &tot);
         for (int j = 0; j < RPW; ++j) {
             if (!ok_of(j)) continue;
-            for (int i = 0; i < 4; ++i) q[pos++] = (uint16_t)(row_of(j) * TW + rx0 + i);
+            for (int i = 0; i < nin; ++i) q[pos++] = (uint16_t)(row_of(j) * TW + rx0 + i);
             // the queue reads G_T from the pixel's slot
-            *reinterpret_cast<uint4*>(&sm.coord[row_of(j) * CROW + rx0]) =
-                *reinterpret_cast<const uint4*>(gtf + (uint32_t)((y0 + row_of(j)) * a.wt + x0 + rx0));
+            *reinterpret_cast<uint4*>(&sm.coord[row_of(j) * CROW + rx0]) = load_gt(j);
         }
         n = tot;
         l = 1;
@@ -547,6 +554,18 @@ __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_const
         const int ry = row_of(j);
         const int64_t o = fpx * frame + (int64_t)((y0 + ry) * wt + (uint32_t)(x0 + rx0));
         const uint4 cv = *reinterpret_cast<const uint4*>(&sm.coord[ry * CROW + rx0]);
+        if (RAG) {  // unaligned row: pixel by pixel, only those inside the row
+            const uint32_t cvv[4] = {cv.x, cv.y, cv.z, cv.w};
+            for (int i = 0; i < nin; ++i) {
+                if (a.coords) st_cs_u32(a.coords + o + i, cvv[i]);
+                if (a.level) a.level[o + i] = lvl[ry * TW + rx0 + i];
+                if (!NOCT && a.ct) {
+                    const uint32_t c = cvv[i];
+                    st_cs_u32(a.ct + 4 * (o + i), __ldg(cs + (PAD ? c : (c >> 16) * ws + (c & 0xFFFFu))));
+                }
+            }
+            continue;
+        }
         if (a.coords) st_cs_u4(a.coords + o, cv);
         if (a.level) st_cs_u32(a.level + o, *reinterpret_cast<const uint32_t*>(&lvl[ry * TW + rx0]));
         if (!NOCT && a.ct) {
@@ -567,7 +586,16 @@ cudaError_t launch_stylize_tiled(const StylizeArgs& a, int n_frames, cudaStream_
     const size_t smem = sizeof(Smem) + (size_t)table_cells(a.L) * (sizeof(uint2) + sizeof(int2)) + (a.level ? TP : 0);
     void (*kern)(StylizeArgs);
     const bool pad = a.exemplar != nullptr;  // the strided exemplar copy: L in 3..5, no weights/labels
-    if (a.ext) {
+    if (a.wt % 4 != 0) {
+        // ragged widths: run-time L, per-pixel row I/O
+        kern = a.ext ? (a.level ? stylize_tiled_kernel<true, true, 0, false, false, true>
+                                : stylize_tiled_kernel<true, false, 0, false, false, true>)
+             : a.level ? (pad ? stylize_tiled_kernel<false, true, 0, true, false, true>
+                              : stylize_tiled_kernel<false, true, 0, false, false, true>)
+             : a.L == 5 && pad ? stylize_tiled_kernel<false, false, 5, true, false, true>
+             : pad ? stylize_tiled_kernel<false, false, 0, true, false, true>
+                   : stylize_tiled_kernel<false, false, 0, false, false, true>;
+    } else if (a.ext) {
         kern = a.level ? stylize_tiled_kernel<true, true, 0, false> : stylize_tiled_kernel<true, false, 0, false>;
     } else if (a.level) {
         kern = a.L == 5 ? (pad ? stylize_tiled_kernel<false, true, 5, true> : stylize_tiled_kernel<false, true, 5, false>)
