@@ -422,7 +422,8 @@ def run_ours(args):
             if p2p:  # the strips are already in rank 0's buffer: order rank 0 after every writer
                 dist.all_reduce(flag)
             elif strip and world > 1:  # the one exchange step: C_T strips -> rank 0 over NCCL
-                sharding.gather_strips(ct[:, rb:re_], HT, world, rank, dst=0, row_axis=1)
+                sharding.gather_strips(ct[:, rb:re_], HT, world, rank, dst=0, row_axis=1,
+                                       out=ct if rank == 0 else None)
             if record:
                 es[4].record(stream)
                 ev["lut"].append((es[0], es[5]))

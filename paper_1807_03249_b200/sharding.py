@@ -9,11 +9,12 @@ level and frame seed, so any partition reproduces the single-GPU result bit for 
 * Strip mode (single-frame latency): each frame is cut into row strips, one per rank.  A rank
   computes its strip through sb_params.row_begin/row_end (the vote's r-row coordinate halo is
   recomputed inside the library, so no halo exchange is needed) and the strips are gathered
-  to the consumer rank -- the one real exchange step.  Two ways: `gather_strips` (one NCCL
-  gather after the compute), or `peer_output` (the consumer's output buffer is mapped into
-  every rank through CUDA IPC and each rank's stylize kernel stores its rows straight into it
-  over NVLink / NVSwitch, so the transfer overlaps the compute tile by tile; a one-element
-  all-reduce then orders the consumer after every writer).
+  to the consumer rank -- the one real exchange step.  Two ways: `gather_strips` (grouped
+  NCCL send/recv after the compute, received straight into the consumer's output rows), or
+  `peer_output` (the consumer's output buffer is mapped into every rank through CUDA IPC and
+  each rank's stylize kernel stores its rows straight into it over NVLink / NVSwitch, so the
+  transfer overlaps the compute tile by tile; a one-element all-reduce then orders the
+  consumer after every writer).
 
 The functions take a torch.distributed process group and work with any backend (NCCL for
 CUDA tensors, gloo for the CPU tests in tests/test_sharding_gloo.py).  Compute is passed in
@@ -42,29 +43,55 @@ def frame_range(n_frames: int, world: int, rank: int) -> tuple[int, int]:
 
 
 def gather_strips(strip: torch.Tensor, ht: int, world: int, rank: int, dst: int = 0, group=None,
-                  row_axis: int = 0):
-    """Gather each rank's row strip (rows along `row_axis`, e.g. [h_k, W, 4] or a batch
-    [B, h_k, W, 4] with row_axis=1) to rank `dst` in ONE collective.
+                  row_axis: int = 0, out: torch.Tensor | None = None):
+    """Gather each rank's row strip to rank `dst` with grouped point-to-point transfers.
 
-    Strips are padded to the largest strip height so the collective sees equal shapes, then
-    trimmed.  Returns the full frame(s) on dst and None elsewhere.
+    `strip` holds this rank's rows along `row_axis` (e.g. [h_k, W, 4], or a batch
+    [B, h_k, W, 4] with row_axis=1), each leading-index slice contiguous.  On dst, `out` (the
+    full frame(s); allocated when None) receives every other rank's strip straight into its own
+    rows -- one recv per rank and leading index, all in one group (one NCCL group call), no
+    padding, no receive buffers, no reassembly copy; dst's own strip is copied only when it is
+    not already a view of `out` (the bench computes it in place).  Returns `out` on dst, None
+    elsewhere.
     """
-    hmax = max(e - b for b, e in (strip_rows(ht, world, r) for r in range(world)))
-    shape = list(strip.shape)
-    shape[row_axis] = hmax
-    pad = torch.zeros(shape, dtype=strip.dtype, device=strip.device)
-    pad.narrow(row_axis, 0, strip.shape[row_axis]).copy_(strip)
+    lead = tuple(strip.shape[:row_axis])
+    n_lead = 1
+    for v in lead:
+        n_lead *= v
+    rest = tuple(strip.shape[row_axis + 1:])
+
+    def rows(t: torch.Tensor, i: int) -> torch.Tensor:
+        """Leading index i (flattened) of t, rows along dimension 0 of the result."""
+        return t.reshape(n_lead, *t.shape[row_axis:])[i]
+
+    b_me, e_me = strip_rows(ht, world, rank)
+    if strip.shape[row_axis] != e_me - b_me:
+        raise ValueError(f"rank {rank} strip has {strip.shape[row_axis]} rows, expected {e_me - b_me}")
+    ops = []
     if rank == dst:
-        bufs = [torch.empty_like(pad) for _ in range(world)]
-        dist.gather(pad, gather_list=bufs, dst=dst, group=group)
-        shape[row_axis] = ht
-        out = torch.empty(shape, dtype=strip.dtype, device=strip.device)
+        if out is None:
+            out = torch.empty(*lead, ht, *rest, dtype=strip.dtype, device=strip.device)
+        mine = out.narrow(row_axis, b_me, e_me - b_me)
+        if mine.data_ptr() != strip.data_ptr():
+            mine.copy_(strip)
         for r in range(world):
+            if r == dst:
+                continue
             b, e = strip_rows(ht, world, r)
-            out.narrow(row_axis, b, e - b).copy_(bufs[r].narrow(row_axis, 0, e - b))
-        return out
-    dist.gather(pad, gather_list=None, dst=dst, group=group)
-    return None
+            if e == b:
+                continue
+            for i in range(n_lead):
+                ops.append(dist.P2POp(dist.irecv, rows(out, i).narrow(0, b, e - b), r, group))
+    elif e_me > b_me:
+        for i in range(n_lead):
+            t = rows(strip, i)
+            if not t.is_contiguous():
+                t = t.contiguous()
+            ops.append(dist.P2POp(dist.isend, t, dst, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    return out if rank == dst else None
 
 
 def _share_cuda_ipc(t: torch.Tensor):
@@ -72,6 +99,13 @@ def _share_cuda_ipc(t: torch.Tensor):
 
 
 def _open_cuda_ipc(handle, shape, dtype):
+    # handle[0] is the owner's device index.  Same device: no peer access needed.  Another
+    # device: torch opens the handle with cudaIpcMemLazyEnablePeerAccess, which enables peer
+    # access from the current device; refuse up front where the hardware cannot do it.
+    here = torch.cuda.current_device()
+    owner = int(handle[0])
+    if owner != here and not torch.cuda.can_device_access_peer(here, owner):
+        raise RuntimeError(f"cuda:{here} cannot access cuda:{owner} as a peer: use the NCCL gather")
     storage = torch.UntypedStorage._new_shared_cuda(*handle)
     out = torch.empty(0, dtype=dtype, device=storage.device)
     strides, acc = [], 1

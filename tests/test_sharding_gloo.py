@@ -140,3 +140,42 @@ def test_strip_mode_peer_output_world2(tmp_path):
         assert p.exitcode == 0
     results = [q.get(timeout=10) for _ in range(world)]
     assert all(results), results
+
+
+def _gather_worker(rank, world, port, q):
+    """gather_strips on a batch [B, H, W, 4] (row_axis=1) with uneven strips and an empty
+    strip (H < world): rank 0 receives straight into its output rows; its own strip is
+    computed in place (a view of the output, so no copy)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ok = True
+        for B, H, W in ((3, 37, 5), (2, 2, 4)):
+            full = torch.arange(B * H * W * 4, dtype=torch.int32).reshape(B, H, W, 4) % 251
+            full = full.to(torch.uint8)
+            b, e = sharding.strip_rows(H, world, rank)
+            if rank == 0:
+                out = torch.zeros_like(full)
+                out[:, b:e] = full[:, b:e]  # "computed in place"
+                got = sharding.gather_strips(out[:, b:e], H, world, rank, dst=0, row_axis=1, out=out)
+                ok &= got is out and torch.equal(out, full)
+            else:
+                ok &= sharding.gather_strips(full[:, b:e].clone(), H, world, rank, dst=0, row_axis=1) is None
+        q.put(bool(ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gather_strips_into_output_rows(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(k, world, port, q)) for k in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    results = [q.get(timeout=10) for _ in range(world)]
+    assert all(results), results
