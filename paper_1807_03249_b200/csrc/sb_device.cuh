@@ -69,6 +69,36 @@ __device__ __forceinline__ void st_cs_u4(void* p, uint4 v) {
                  "r"(v.w)
                  : "memory");
 }
+__device__ __forceinline__ void st_cs_u2(void* p, uint32_t a, uint32_t b) {
+    asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(a), "r"(b) : "memory");
+}
+// 4 consecutive words at any 4-byte-aligned address: one 16-byte, two 8-byte or four 4-byte
+// streaming stores, whichever the address allows (rows of a ragged-width image)
+__device__ __forceinline__ void st_cs_4w(uint32_t* p, uint4 v) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    if ((a & 15u) == 0) {
+        asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                     : "memory");
+    } else if ((a & 7u) == 0) {
+        st_cs_u2(p, v.x, v.y);
+        st_cs_u2(p + 2, v.z, v.w);
+    } else {
+        asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v.x) : "memory");
+        asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p + 1), "r"(v.y) : "memory");
+        asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p + 2), "r"(v.z) : "memory");
+        asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p + 3), "r"(v.w) : "memory");
+    }
+}
+// ... and the matching loads
+__device__ __forceinline__ uint4 ld_4w(const uint32_t* p) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    if ((a & 15u) == 0) return *reinterpret_cast<const uint4*>(p);
+    if ((a & 7u) == 0) {
+        const uint2 u = *reinterpret_cast<const uint2*>(p), w = *reinterpret_cast<const uint2*>(p + 2);
+        return make_uint4(u.x, u.y, w.x, w.y);
+    }
+    return make_uint4(p[0], p[1], p[2], p[3]);
+}
 __device__ __forceinline__ void st_cs_u32(void* p, uint32_t v) {
     asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

@@ -338,7 +338,8 @@ __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_const
     auto load_gt = [&](int j) {
         const uint32_t* p = gtf + (uint32_t)((y0 + row_of(j)) * a.wt + x0 + rx0);
         if (!RAG) return *reinterpret_cast<const uint4*>(p);
-        return make_uint4(__ldg(p), nin > 1 ? __ldg(p + 1) : 0u, nin > 2 ? __ldg(p + 2) : 0u, nin > 3 ? __ldg(p + 3) : 0u);
+        if (nin == 4) return ld_4w(p);  // widest load the row's alignment allows
+        return make_uint4(__ldg(p), nin > 1 ? __ldg(p + 1) : 0u, nin > 2 ? __ldg(p + 2) : 0u, 0u);
     };
     uint4 gp[RPW];
 #pragma unroll
@@ -554,7 +555,20 @@ __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_const
         const int ry = row_of(j);
         const int64_t o = fpx * frame + (int64_t)((y0 + ry) * wt + (uint32_t)(x0 + rx0));
         const uint4 cv = *reinterpret_cast<const uint4*>(&sm.coord[ry * CROW + rx0]);
-        if (RAG) {  // unaligned row: pixel by pixel, only those inside the row
+        if (RAG && nin == 4) {  // a whole group of an unaligned row: the widest stores its address allows
+            if (a.coords) st_cs_4w(a.coords + o, cv);
+            if (a.level) {
+                for (int i = 0; i < 4; ++i) a.level[o + i] = lvl[ry * TW + rx0 + i];
+            }
+            if (!NOCT && a.ct) {
+                auto idx = [&](uint32_t c) { return PAD ? c : (c >> 16) * ws + (c & 0xFFFFu); };
+                st_cs_4w(reinterpret_cast<uint32_t*>(a.ct) + o,
+                         make_uint4(__ldg(cs + idx(cv.x)), __ldg(cs + idx(cv.y)), __ldg(cs + idx(cv.z)),
+                                    __ldg(cs + idx(cv.w))));
+            }
+            continue;
+        }
+        if (RAG) {  // the row's last, partial group: pixel by pixel, only those inside the row
             const uint32_t cvv[4] = {cv.x, cv.y, cv.z, cv.w};
             for (int i = 0; i < nin; ++i) {
                 if (a.coords) st_cs_u32(a.coords + o + i, cvv[i]);
