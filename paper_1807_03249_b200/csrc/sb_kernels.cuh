@@ -62,6 +62,7 @@ cudaError_t launch_prepare_exemplar(const uint8_t* cs, const uint8_t* gs, int ws
 cudaError_t launch_stylize_naive(const StylizeArgs& a, int n_frames, cudaStream_t st, int* launches);
 cudaError_t launch_stylize_tiled(const StylizeArgs& a, int n_frames, cudaStream_t st, int* launches);
 cudaError_t launch_vote(const VoteArgs& a, int n_frames, cudaStream_t st, int* launches);
+cudaError_t launch_vote_hist(const VoteArgs& a, int n_frames, cudaStream_t st, int* launches);
 cudaError_t launch_vote_peel(const VoteArgs& a, int n_frames, cudaStream_t st, int* launches);
 
 }  // namespace sb

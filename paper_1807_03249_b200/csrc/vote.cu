@@ -29,8 +29,14 @@
 // source bounds tests on packed coordinates (x | y<<16; for W, H <= 32767 and |d| <= 2r the
 // packed sum src(q) + (p-q) never carries between fields and any position left of / above
 // the source wraps to a field >= 0xFFF0, which the bounds test rejects).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <map>
+#include <mutex>
 
 #include "sb_kernels.cuh"
 
@@ -79,89 +85,48 @@ __device__ __forceinline__ void swar_add(uint32_t c, uint32_t& lo, uint32_t& hi)
 }
 }  // namespace
 
+// Tile geometry and the shared scratch of one tile (besides the staged coordinates).
+template <int R>
+struct VoteGeom {
+    static constexpr int SW = TW + 2 * R, SH = TH + 2 * R;
+    static constexpr int KR = (R + 3) / 4;    // 16-byte words covering the halo
+    static constexpr int OFF = 4 * KR;        // tile column x is stored at sc[.][OFF + x]
+    static constexpr int SWP = OFF + TW + OFF;  // 16-byte aligned rows
+};
+
+template <int R>
+struct VoteShared {
+    static constexpr int SH = VoteGeom<R>::SH;
+    uint8_t seg[SH][NG];        // nibble: which of the group's 4 row segments are one chunk
+    uint8_t seg3[SH][NG];       // nibble: which of them have three or more runs
+    uint32_t hl[SH][6];         // row link bits: bit x+32 <=> position x+1 continues x
+    __align__(16) uint32_t outc[TH][TW];
+    uint16_t queue[TH * TW];    // two-run pixels from the front, others from the back
+    int qn, qn3;
+};
+
+// The vote of one tile whose coordinates (tile + r halo, kOutside outside the target) are
+// staged in sc; fast: the fast-tile margin holds for every staged position.  S.qn and S.qn3
+// are zero and ordered before the call by a CTA barrier.
 // PAD: C_S is read from the strided exemplar copy (rows of 2^16 pixels, sb_prepare_exemplar),
 // where a packed coordinate x | y<<16 is its own index: the "linear" source indices below are
 // then the packed values themselves (row stride 65536) and the conversion pass disappears.
 template <int R, bool PAD>
-__global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteArgs a) {
-    constexpr int SW = TW + 2 * R, SH = TH + 2 * R;
-    constexpr int KR = (R + 3) / 4;           // 16-byte words covering the halo
-    constexpr int OFF = 4 * KR;               // tile column x is stored at sc[.][OFF + x]
-    constexpr int SWP = OFF + TW + OFF;       // 16-byte aligned rows
-    __shared__ __align__(16) uint32_t sc[SH][SWP];
-    __shared__ uint8_t seg[SH][NG];        // nibble: which of the group's 4 row segments are one chunk
-    __shared__ uint8_t seg3[SH][NG];       // nibble: which of them have three or more runs
-    __shared__ uint32_t hl[SH][6];         // row link bits: bit x+32 <=> position x+1 continues x
-    __shared__ __align__(16) uint32_t outc[TH][TW];
-    __shared__ uint16_t queue[TH * TW];    // two-run pixels from the front, others from the back
-    __shared__ int qn, qn3;
-
-    const int tiles_x = (a.wt + TW - 1) / TW;
-    const int x0 = (blockIdx.x % tiles_x) * TW;
-    const int y0 = a.row_begin + (blockIdx.x / tiles_x) * TH;
+__device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[VoteGeom<R>::SWP], VoteShared<R>& S,
+                                          int x0, int y0, int frame, bool fast) {
+    constexpr int SH = VoteGeom<R>::SH, KR = VoteGeom<R>::KR, OFF = VoteGeom<R>::OFF, SWP = VoteGeom<R>::SWP;
+    auto& seg = S.seg;
+    auto& seg3 = S.seg3;
+    auto& hl = S.hl;
+    auto& outc = S.outc;
+    auto& queue = S.queue;
+    int& qn = S.qn;
+    int& qn3 = S.qn3;
     const int64_t fpx = (int64_t)a.wt * a.ht;
-    const uint32_t* __restrict__ cf = a.coords + fpx * blockIdx.y;
     const uint32_t* __restrict__ cs = reinterpret_cast<const uint32_t*>(PAD ? a.cs_pad : a.cs);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t ws = (uint32_t)a.ws, hs = (uint32_t)a.hs;
     const uint32_t wsl = PAD ? 65536u : ws;  // row stride of the "linear" source index
-
-    if (threadIdx.x == 0) qn = qn3 = 0;
-    // ---- stage coords (tile + halo), outside the target -> kOutside; test the fast-tile margin
-    bool fast_mine = true;
-    auto stage = [&](int yy, int x, uint32_t v, bool in) {  // x: tile column (-R .. TW-1+R)
-        if (in) {
-            const uint32_t sx = v & 0xFFFFu, sy = v >> 16;
-            fast_mine &= (sx >= (uint32_t)R) & (sx + (uint32_t)R < ws) & (sy >= (uint32_t)R) & (sy + (uint32_t)R < hs);
-        } else {
-            v = kOutside;
-            fast_mine = false;
-        }
-        sc[yy][OFF + x] = v;
-    };
-    if ((a.wt & 3) == 0) {
-        // centre columns: one 16-byte load per 4 pixels
-        for (int i = threadIdx.x; i < SH * NG; i += NT) {
-            const int yy = i / NG, gg = i - yy * NG;
-            const int gx = x0 + 4 * gg, gy = y0 - R + yy;
-            const bool rowin = gy >= 0 && gy < a.ht;
-            if (rowin && gx + 3 < a.wt) {
-                const uint4 v = *reinterpret_cast<const uint4*>(cf + (int64_t)gy * a.wt + gx);
-                uint32_t m = 0;
-                const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint32_t sx = vv[k] & 0xFFFFu, sy = vv[k] >> 16;
-                    m |= (uint32_t)((sx < (uint32_t)R) | (sx + (uint32_t)R >= ws) | (sy < (uint32_t)R) |
-                                    (sy + (uint32_t)R >= hs));
-                }
-                fast_mine &= (m == 0);
-                *reinterpret_cast<uint4*>(&sc[yy][OFF + 4 * gg]) = v;
-            } else {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const bool in = rowin && gx + k < a.wt;
-                    stage(yy, 4 * gg + k, in ? __ldg(cf + (int64_t)gy * a.wt + gx + k) : 0u, in);
-                }
-            }
-        }
-        // halo columns
-        for (int i = threadIdx.x; i < SH * 2 * R; i += NT) {
-            const int yy = i / (2 * R), k = i - yy * (2 * R);
-            const int x = k < R ? k - R : TW + (k - R);
-            const int gx = x0 + x, gy = y0 - R + yy;
-            const bool in = gx >= 0 && gx < a.wt && gy >= 0 && gy < a.ht;
-            stage(yy, x, in ? __ldg(cf + (int64_t)gy * a.wt + gx) : 0u, in);
-        }
-    } else {
-        for (int i = threadIdx.x; i < SW * SH; i += NT) {
-            const int yy = i / SW, xx = i - yy * SW;
-            const int gx = x0 - R + xx, gy = y0 - R + yy;
-            const bool in = gx >= 0 && gx < a.wt && gy >= 0 && gy < a.ht;
-            stage(yy, xx - R, in ? __ldg(cf + (int64_t)gy * a.wt + gx) : 0u, in);
-        }
-    }
-    const bool fast = __syncthreads_and(fast_mine) != 0;
 
     const int g = lane;                  // this thread's 4-pixel group column (pixels 4g..4g+3)
     if (fast) {
@@ -368,7 +333,7 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteAr
         const int py = y0 + ry;
         const int gx0 = x0 + 4 * g;
         if (py >= a.row_end || gx0 >= a.wt) continue;
-        const int64_t off = fpx * blockIdx.y + (int64_t)py * a.wt + gx0;
+        const int64_t off = fpx * frame + (int64_t)py * a.wt + gx0;
         const uint4 o = *reinterpret_cast<const uint4*>(&outc[ry][4 * g]);
         if (vec) {
             st_cs_u4(a.ct + 4 * off, o);
@@ -378,6 +343,192 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteAr
             for (int k = 0; k < 4; ++k)
                 if (gx0 + k < a.wt) st_cs_u32(a.ct + 4 * (off + k), ov[k]);
         }
+    }
+}
+
+
+// The grid-per-tile kernel: coordinates staged with 16-byte loads (any width).
+template <int R, bool PAD>
+__global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteArgs a) {
+    constexpr int SW = VoteGeom<R>::SW, SH = VoteGeom<R>::SH, OFF = VoteGeom<R>::OFF, SWP = VoteGeom<R>::SWP;
+    __shared__ __align__(16) uint32_t sc[SH][SWP];
+    __shared__ VoteShared<R> S;
+    const int tiles_x = (a.wt + TW - 1) / TW;
+    const int x0 = (blockIdx.x % tiles_x) * TW;
+    const int y0 = a.row_begin + (blockIdx.x / tiles_x) * TH;
+    const int64_t fpx = (int64_t)a.wt * a.ht;
+    const uint32_t* __restrict__ cf = a.coords + fpx * blockIdx.y;
+    const uint32_t ws = (uint32_t)a.ws, hs = (uint32_t)a.hs;
+    if (threadIdx.x == 0) S.qn = S.qn3 = 0;
+    // ---- stage coords (tile + halo), outside the target -> kOutside; test the fast-tile margin
+    bool fast_mine = true;
+    auto stage = [&](int yy, int x, uint32_t v, bool in) {  // x: tile column (-R .. TW-1+R)
+        if (in) {
+            const uint32_t sx = v & 0xFFFFu, sy = v >> 16;
+            fast_mine &= (sx >= (uint32_t)R) & (sx + (uint32_t)R < ws) & (sy >= (uint32_t)R) & (sy + (uint32_t)R < hs);
+        } else {
+            v = kOutside;
+            fast_mine = false;
+        }
+        sc[yy][OFF + x] = v;
+    };
+    if ((a.wt & 3) == 0) {
+        // centre columns: one 16-byte load per 4 pixels
+        for (int i = threadIdx.x; i < SH * NG; i += NT) {
+            const int yy = i / NG, gg = i - yy * NG;
+            const int gx = x0 + 4 * gg, gy = y0 - R + yy;
+            const bool rowin = gy >= 0 && gy < a.ht;
+            if (rowin && gx + 3 < a.wt) {
+                const uint4 v = *reinterpret_cast<const uint4*>(cf + (int64_t)gy * a.wt + gx);
+                uint32_t m = 0;
+                const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t sx = vv[k] & 0xFFFFu, sy = vv[k] >> 16;
+                    m |= (uint32_t)((sx < (uint32_t)R) | (sx + (uint32_t)R >= ws) | (sy < (uint32_t)R) |
+                                    (sy + (uint32_t)R >= hs));
+                }
+                fast_mine &= (m == 0);
+                *reinterpret_cast<uint4*>(&sc[yy][OFF + 4 * gg]) = v;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const bool in = rowin && gx + k < a.wt;
+                    stage(yy, 4 * gg + k, in ? __ldg(cf + (int64_t)gy * a.wt + gx + k) : 0u, in);
+                }
+            }
+        }
+        // halo columns
+        for (int i = threadIdx.x; i < SH * 2 * R; i += NT) {
+            const int yy = i / (2 * R), k = i - yy * (2 * R);
+            const int x = k < R ? k - R : TW + (k - R);
+            const int gx = x0 + x, gy = y0 - R + yy;
+            const bool in = gx >= 0 && gx < a.wt && gy >= 0 && gy < a.ht;
+            stage(yy, x, in ? __ldg(cf + (int64_t)gy * a.wt + gx) : 0u, in);
+        }
+    } else {
+        for (int i = threadIdx.x; i < SW * SH; i += NT) {
+            const int yy = i / SW, xx = i - yy * SW;
+            const int gx = x0 - R + xx, gy = y0 - R + yy;
+            const bool in = gx >= 0 && gx < a.wt && gy >= 0 && gy < a.ht;
+            stage(yy, xx - R, in ? __ldg(cf + (int64_t)gy * a.wt + gx) : 0u, in);
+        }
+    }
+    const bool fast = __syncthreads_and(fast_mine) != 0;
+
+    vote_tile<R, PAD>(a, sc, S, x0, y0, blockIdx.y, fast);
+}
+
+
+// ---- TMA-fed persistent kernel (rows of 16-byte multiple strides, i.e. wt % 4 == 0) ----
+// One CTA per resident slot loops over tiles (frame-major); the staged coordinates of tile k+1
+// are fetched by the Tensor Memory Accelerator (one 3-D box [frame][SH rows][SWP columns],
+// zero-filled outside the tensor) into the other of two shared buffers while tile k is voted,
+// so the HBM latency of the coordinates no longer stalls the CTA at its staging barrier.
+// Completion: one mbarrier per buffer (expect_tx = box bytes), waited with parity.
+namespace {
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// Thread 0: arm the buffer's barrier with the box bytes and start the 3-D box load.
+__device__ __forceinline__ void tma_box3(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar,
+                                         uint32_t bytes) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic accesses of dst first
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+}  // namespace
+
+template <int R, bool PAD>
+__global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2))
+    vote_tma_kernel(const VoteArgs a, const __grid_constant__ CUtensorMap tm, int tiles_x, int tiles_per_frame,
+                    int n_tiles) {
+    constexpr int SH = VoteGeom<R>::SH, OFF = VoteGeom<R>::OFF, SWP = VoteGeom<R>::SWP;
+    constexpr uint32_t kBox = SH * SWP * 4;
+    __shared__ __align__(128) uint32_t sc0[SH][SWP];
+    __shared__ __align__(128) uint32_t sc1[SH][SWP];
+    __shared__ __align__(8) uint64_t mbar[2];
+    __shared__ VoteShared<R> S;
+    const int tid = threadIdx.x;
+    const uint32_t ws = (uint32_t)a.ws, hs = (uint32_t)a.hs;
+    auto origin = [&](int t, int& x0, int& y0, int& f) {
+        f = t / tiles_per_frame;
+        const int r = t - f * tiles_per_frame;
+        x0 = (r % tiles_x) * TW;
+        y0 = a.row_begin + (r / tiles_x) * TH;
+    };
+    auto fetch = [&](int t, void* dst, uint64_t* bar) {
+        int x0, y0, f;
+        origin(t, x0, y0, f);
+        tma_box3(dst, &tm, x0 - OFF, y0 - R, f, bar, kBox);
+    };
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if ((int)blockIdx.x < n_tiles) fetch(blockIdx.x, sc0, &mbar[0]);
+    }
+    __syncthreads();
+    uint32_t parity = 0;  // bit b: phase of buffer b
+    int k = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
+        const int b = k & 1;
+        uint32_t(*sc)[SWP] = b ? sc1 : sc0;
+        if (tid == 0) {
+            const int tn = t + gridDim.x;  // the next tile into the other buffer (free since the last barrier)
+            if (tn < n_tiles) fetch(tn, b ? (void*)sc0 : (void*)sc1, &mbar[b ^ 1]);
+            S.qn = S.qn3 = 0;
+        }
+        int x0, y0, f;
+        origin(t, x0, y0, f);
+        mbar_wait(&mbar[b], (parity >> b) & 1u);
+        parity ^= 1u << b;
+        // positions outside the target were zero-filled: mark them (only tiles at the frame edge);
+        // the fast-tile margin over every staged word (the extra alignment columns included)
+        bool fast_mine = true;
+        const bool edge = x0 - R < 0 || x0 + TW + R > a.wt || y0 - R < 0 || y0 + TH + R > a.ht;
+        for (int i = tid; i < SH * (SWP / 4); i += NT) {
+            const int yy = i / (SWP / 4), c4 = i - yy * (SWP / 4);
+            uint4 v = *reinterpret_cast<const uint4*>(&sc[yy][4 * c4]);
+            uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+            uint32_t m = 0;
+            bool out = false;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (edge) {
+                    const int gx = x0 - OFF + 4 * c4 + j, gy = y0 - R + yy;
+                    if (gx < 0 || gx >= a.wt || gy < 0 || gy >= a.ht) {
+                        vv[j] = kOutside;
+                        out = true;
+                    }
+                }
+                const uint32_t sx = vv[j] & 0xFFFFu, sy = vv[j] >> 16;
+                m |= (uint32_t)((sx < (uint32_t)R) | (sx + (uint32_t)R >= ws) | (sy < (uint32_t)R) |
+                                (sy + (uint32_t)R >= hs));
+            }
+            fast_mine &= (m == 0);
+            if (out) *reinterpret_cast<uint4*>(&sc[yy][4 * c4]) = make_uint4(vv[0], vv[1], vv[2], vv[3]);
+        }
+        const bool fast = __syncthreads_and(fast_mine) != 0;
+        vote_tile<R, PAD>(a, sc, S, x0, y0, f, fast);
+        __syncthreads();  // sc and S are free for the tiles to come
     }
 }
 
@@ -399,13 +550,99 @@ static void launch_r(const VoteArgs& a, dim3 grid, cudaStream_t st) {
     kern<<<grid, NT, 0, st>>>(a);
 }
 
-cudaError_t launch_vote(const VoteArgs& a, int n_frames, cudaStream_t st, int* launches) {
-    // SB_VOTE=peel: the peel vote of vote_peel.cu for r = 1, 2 (A/B; measured slower)
-    static const bool peel = [] {
-        const char* e = getenv("SB_VOTE");
-        return e && strcmp(e, "peel") == 0;
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link needed).
+static PFN_cuTensorMapEncodeTiled encode_fn() {
+    static PFN_cuTensorMapEncodeTiled fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(p);
     }();
-    if ((a.r == 1 || a.r == 2) && peel) return launch_vote_peel(a, n_frames, st, launches);
+    return fn;
+}
+
+// Resident CTAs per SM of a kernel (cached per device and kernel).
+static int resident_ctas(const void* kern, int threads) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(dev, kern);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, 0) != cudaSuccess || n < 1) n = 1;
+    cache[key] = n;
+    return n;
+}
+
+// The TMA-fed persistent launch; false when it does not apply (ragged rows, no driver entry
+// point, tensor-map encoding refused), in which case the caller uses the grid-per-tile kernel.
+template <int R>
+static bool launch_tma_r(const VoteArgs& a, int n_frames, cudaStream_t st) {
+    if (a.wt % 4 != 0 || !encode_fn()) return false;
+    CUtensorMap tm;
+    const cuuint64_t dims[3] = {(cuuint64_t)a.wt, (cuuint64_t)a.ht, (cuuint64_t)n_frames};
+    const cuuint64_t strides[2] = {(cuuint64_t)a.wt * 4, (cuuint64_t)a.wt * a.ht * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)VoteGeom<R>::SWP, (cuuint32_t)VoteGeom<R>::SH, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    if (encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint32_t*>(a.coords), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    const int tiles_x = (a.wt + TW - 1) / TW;
+    const int tiles_per_frame = tiles_x * ((a.row_end - a.row_begin + TH - 1) / TH);
+    const int n_tiles = tiles_per_frame * n_frames;
+    auto kern = a.cs_pad ? vote_tma_kernel<R, true> : vote_tma_kernel<R, false>;
+    // two staging buffers: more shared memory per CTA than the grid-per-tile kernel, so its
+    // carve-out would cost residency; SB_VOTE_TMA_CARVEOUT (percent) overrides the default
+    static const int carve = [] {
+        const char* e = getenv("SB_VOTE_TMA_CARVEOUT");
+        return e ? atoi(e) : -1;
+    }();
+    ensure_carveout(reinterpret_cast<const void*>(kern), carve);
+    const int grid = std::min(n_tiles, sm_count() * resident_ctas(reinterpret_cast<const void*>(kern), NT));
+    kern<<<grid, NT, 0, st>>>(a, tm, tiles_x, tiles_per_frame, n_tiles);
+    return true;
+}
+
+cudaError_t launch_vote(const VoteArgs& a, int n_frames, cudaStream_t st, int* launches) {
+    // A/B alternatives for r = 1, 2 (measured slower): SB_VOTE=peel the peel vote
+    // of vote_peel.cu, SB_VOTE=hist the offset-histogram vote of vote_hist.cu.
+    static const int which = [] {
+        const char* e = getenv("SB_VOTE");
+        if (e && strcmp(e, "peel") == 0) return 1;
+        if (e && strcmp(e, "hist") == 0) return 2;
+        return 0;
+    }();
+    if ((a.r == 1 || a.r == 2) && which == 1) return launch_vote_peel(a, n_frames, st, launches);
+    if ((a.r == 1 || a.r == 2) && which == 2) return launch_vote_hist(a, n_frames, st, launches);
+    // the TMA-fed persistent kernel unless SB_VOTE_TMA=0 (A/B) or it does not apply
+    static const bool tma = [] {
+        const char* e = getenv("SB_VOTE_TMA");
+        return !(e && strcmp(e, "0") == 0);
+    }();
+    if (tma && n_frames > 0) {
+        bool done = false;
+        switch (a.r) {
+            case 0: done = launch_tma_r<0>(a, n_frames, st); break;
+            case 1: done = launch_tma_r<1>(a, n_frames, st); break;
+            case 2: done = launch_tma_r<2>(a, n_frames, st); break;
+            case 3: done = launch_tma_r<3>(a, n_frames, st); break;
+            case 4: done = launch_tma_r<4>(a, n_frames, st); break;
+            case 5: done = launch_tma_r<5>(a, n_frames, st); break;
+            case 6: done = launch_tma_r<6>(a, n_frames, st); break;
+            case 7: break;  // two r = 7 buffers exceed the 48 KB of static shared memory
+            default: return cudaErrorInvalidValue;
+        }
+        if (done) {
+            *launches += 1;
+            return cudaPeekAtLastError();
+        }
+    }
     const int tiles = ((a.wt + TW - 1) / TW) * ((a.row_end - a.row_begin + TH - 1) / TH);
     dim3 grid((unsigned)tiles, (unsigned)n_frames);
     switch (a.r) {
