@@ -620,10 +620,11 @@ cudaError_t launch_vote(const VoteArgs& a, int n_frames, cudaStream_t st, int* l
     }();
     if ((a.r == 1 || a.r == 2) && which == 1) return launch_vote_peel(a, n_frames, st, launches);
     if ((a.r == 1 || a.r == 2) && which == 2) return launch_vote_hist(a, n_frames, st, launches);
-    // the TMA-fed persistent kernel unless SB_VOTE_TMA=0 (A/B) or it does not apply
+    // SB_VOTE_TMA=1: the TMA-fed persistent kernel where it applies (A/B; measured slower,
+    // DESIGN.md 11)
     static const bool tma = [] {
         const char* e = getenv("SB_VOTE_TMA");
-        return !(e && strcmp(e, "0") == 0);
+        return e && strcmp(e, "1") == 0;
     }();
     if (tma && n_frames > 0) {
         bool done = false;

@@ -1,6 +1,6 @@
-"""The A/B vote kernels selected by SB_VOTE (peel: vote_peel.cu, hist: vote_hist.cu; r = 1, 2) are
-bit-exact against the oracle too.  SB_VOTE is read once per process, so each variant runs in
-its own subprocess on the distinct-offset fields of test_parity_gpu (chunk sizes 1..32, frame
+"""The A/B vote kernels selected by SB_VOTE (peel: vote_peel.cu, hist: vote_hist.cu; r = 1, 2) and
+SB_VOTE_TMA=1 (the TMA-fed persistent kernel of vote.cu) are bit-exact against the oracle too.
+The switches are read once per process, so each variant runs in its own subprocess on the distinct-offset fields of test_parity_gpu (chunk sizes 1..32, frame
 borders, ragged widths, sources at the exemplar border)."""
 import os
 import subprocess
@@ -49,8 +49,9 @@ sys.exit(1 if bad else 0)
 '''
 
 
-@pytest.mark.parametrize("variant", ["peel", "hist"])
+@pytest.mark.parametrize("variant", ["SB_VOTE=peel", "SB_VOTE=hist", "SB_VOTE_TMA=1"])
 def test_vote_variant_exact(variant):
-    env = dict(os.environ, SB_VOTE=variant)
+    k, v = variant.split("=")
+    env = dict(os.environ, **{k: v})
     r = subprocess.run([sys.executable, "-c", CHILD], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
