@@ -23,7 +23,9 @@
  *  - Images are row-major, contiguous, 4 bytes per pixel (uint8 x4; RGBA8 colours,
  *    up to 4 guide channels), pixel (x,y) at byte offset 4*(y*W + x).  Frames of a batch
  *    are contiguous: frame i starts at byte 4*W*H*i.  Base pointers must be 16-byte
- *    aligned.  1 <= W, H <= 32767 (packed 16-bit coordinates never carry, see vote.cu).
+ *    aligned.  1 <= W, H <= 65535 (SB_MAX_DIM).  Sides up to 32767 run on the tiled
+ *    packed-coordinate kernels; larger ones on per-pixel kernels with signed coordinates
+ *    (identical results, slower).
  *  - Source coordinates are packed x | y << 16 (uint32) in SOURCE space.
  *  - The LUT has 65536 uint32 entries indexed by key = G[0] | G[1] << 8 (the first two
  *    guide channels, the paper's "two values").
@@ -72,8 +74,11 @@ typedef enum {
                                 and ct_host receives C_T channels 0..2 -- so 3/4 of the PCIe
                                 bytes move; the device kernels unpack/pack them.  wt % 4 == 0. */
 
-#define SB_MAX_LEVELS 12      /* level l uses spacing h = 2^l, l in [1, SB_MAX_LEVELS]       */
-#define SB_MAX_RADIUS 7       /* voting radius r in [0, SB_MAX_RADIUS]; (2r+1)^2*255 < 2^16   */
+#define SB_MAX_DIM 65535      /* image sides W, H in [1, SB_MAX_DIM] (target and source)      */
+#define SB_MAX_LEVELS 15      /* level l uses spacing h = 2^l, l in [1, SB_MAX_LEVELS]; L <= 9
+                                 on the tiled kernel, L in 10..15 on the per-pixel kernel     */
+#define SB_MAX_RADIUS 8       /* voting radius r in [0, SB_MAX_RADIUS]; r <= 7 on the 16-bit
+                                 SWAR vote kernels, r = 8 on the 32-bit per-pixel vote       */
 
 typedef struct {
     /* t: the threshold of Alg. 2 line 385 ("e < t"), in 8-bit guide units.  The error e is

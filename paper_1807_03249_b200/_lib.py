@@ -19,8 +19,8 @@ SB_NO_COLOR = 0x2
 SB_LABEL = 0x4
 SB_LUT_RGB = 0x8
 SB_HOST_RGB = 0x10
-SB_MAX_LEVELS = 12
-SB_MAX_RADIUS = 7
+SB_MAX_LEVELS = 15
+SB_MAX_RADIUS = 8
 
 # every symbol include/styleblit.h declares
 EXPORTS = (

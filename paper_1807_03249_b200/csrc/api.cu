@@ -27,7 +27,7 @@ sb_status cuda_fail(cudaError_t e, const char* where) {
     return fail(SB_ECUDA, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
 }
 
-constexpr int kMaxDim = 32767;
+constexpr int kMaxDim = SB_MAX_DIM;
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -39,14 +39,16 @@ sb_status check_dims(const char* name, int32_t w, int32_t h) {
 
 // Which stylize kernel: the tiled kernel (any width; ragged widths take its per-pixel row I/O
 // instantiation) needs L <= 9 (its tabled NearestSeed keys 1024 d + code fit 32 bits for
-// h <= 2^9, stylize.cu); SB_KERNEL=naive selects the one-thread-per-pixel kernel (A/B).
-bool use_naive(int32_t wt, int32_t L) {
+// h <= 2^9, stylize.cu) and every image side <= 32767 (packed candidate arithmetic); the
+// one-thread-per-pixel kernel (signed coordinates, 64-bit distances) serves the rest.
+// SB_KERNEL=naive selects it always (A/B).
+bool use_naive(const sb::StylizeArgs& a) {
     static const int forced = [] {
         const char* e = getenv("SB_KERNEL");
         return (e && strcmp(e, "naive") == 0) ? 1 : 0;
     }();
-    (void)wt;
-    return forced || L > 9;
+    const int big = sb::kPackedMaxDim;
+    return forced || a.L > 9 || a.wt > big || a.ht > big || a.ws > big || a.hs > big;
 }
 
 struct Prepared {
@@ -147,7 +149,7 @@ sb_status launch_frames(Prepared& p, int n_frames, const uint32_t* frame_seeds, 
         a.has_seeds = frame_seeds ? 1 : 0;
         a.seed_base = seed_base_f0 + (uint32_t)f0;
         if (frame_seeds) memcpy(a.seeds, frame_seeds + f0, sizeof(uint32_t) * nf);
-        cudaError_t e = use_naive(a.wt, a.L) ? sb::launch_stylize_naive(a, nf, st, &g_launches)
+        cudaError_t e = use_naive(a) ? sb::launch_stylize_naive(a, nf, st, &g_launches)
                                         : sb::launch_stylize_tiled(a, nf, st, &g_launches);
         if (e != cudaSuccess) return cuda_fail(e, "stylize launch");
         if (p.vote) {

@@ -30,11 +30,12 @@ __global__ void __launch_bounds__(256) lut3_init_kernel(uint32_t* __restrict__ s
     reinterpret_cast<uint4*>(site)[i] = make_uint4(kNone, kNone, kNone, kNone);
 }
 
-__global__ void __launch_bounds__(256) lut3_sites_kernel(const uint32_t* __restrict__ gs, int n,
+__global__ void __launch_bounds__(256) lut3_sites_kernel(const uint32_t* __restrict__ gs, uint32_t n,
                                                          uint32_t* __restrict__ site) {
     const int lane = threadIdx.x & 31;
-    for (int i0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; i0 < n; i0 += gridDim.x * blockDim.x) {
-        const int i = i0 + lane;
+    // pixel indices up to 65535^2 - 1 < 2^32 - 1 (the empty-site marker): 64-bit loop counter
+    for (uint64_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; i0 < n; i0 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = i0 + (uint64_t)lane;
         const bool valid = i < n;
         const uint32_t key = valid ? (__ldg(gs + i) & 0xFFFFFFu) : 0x1000000u + lane;
         const unsigned peers = __match_any_sync(0xFFFFFFFFu, key);
@@ -101,7 +102,7 @@ cudaError_t launch_build_lut3(const uint8_t* gs, int ws, int hs, uint32_t* lut3,
     uint32_t* site = lut3;  // the output doubles as the site table
     uint2* d = static_cast<uint2*>(workspace);
     lut3_init_kernel<<<N / 4 / 256, 256, 0, st>>>(site);
-    const int n = ws * hs;
+    const uint32_t n = (uint32_t)ws * (uint32_t)hs;
     int blocks = (n + 255) / 256;
     if (blocks > sm_count() * 16) blocks = sm_count() * 16;
     lut3_sites_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(gs), n, site);

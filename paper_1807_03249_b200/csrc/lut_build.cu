@@ -25,11 +25,12 @@ __global__ void __launch_bounds__(256) lut_init_kernel(uint32_t* __restrict__ si
     reinterpret_cast<uint4*>(site)[i] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
 }
 
-__global__ void __launch_bounds__(256) lut_sites_kernel(const uint32_t* __restrict__ gs, int n,
+__global__ void __launch_bounds__(256) lut_sites_kernel(const uint32_t* __restrict__ gs, uint32_t n,
                                                         uint32_t* __restrict__ site) {
     const int lane = threadIdx.x & 31;
-    for (int i0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; i0 < n; i0 += gridDim.x * blockDim.x) {
-        const int i = i0 + lane;
+    // pixel indices up to 65535^2 - 1 < 2^32 - 1 (the empty-site marker): 64-bit loop counter
+    for (uint64_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; i0 < n; i0 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = i0 + (uint64_t)lane;
         const bool valid = i < n;
         const uint32_t key = valid ? (__ldg(gs + i) & 0xFFFFu) : 0x10000u + lane;
         // lanes holding the same key: the lowest lane has the smallest pixel index
@@ -140,7 +141,7 @@ cudaError_t launch_build_lut(const uint8_t* gs, int ws, int hs, uint32_t* lut, v
                              cudaStream_t st, int* launches) {
     uint32_t* site = static_cast<uint32_t*>(workspace);
     lut_init_kernel<<<65536 / 4 / 256, 256, 0, st>>>(site);
-    const int n = ws * hs;
+    const uint32_t n = (uint32_t)ws * (uint32_t)hs;
     int blocks = (n + 255) / 256;
     if (blocks > sm_count() * 16) blocks = sm_count() * 16;
     lut_sites_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(gs), n, site);

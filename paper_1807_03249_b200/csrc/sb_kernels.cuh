@@ -5,7 +5,8 @@
 namespace sb {
 
 constexpr int kSeedsPerLaunch = 512;  // frames per launch (per-frame seeds travel as params)
-#define SB_MAX_LEVELS_DEV 12           // == SB_MAX_LEVELS of include/styleblit.h
+#define SB_MAX_LEVELS_DEV 15           // == SB_MAX_LEVELS of include/styleblit.h
+constexpr int kPackedMaxDim = 32767;  // packed-arithmetic kernels: every image side <= this
 
 struct StylizeArgs {
     const uint8_t* cs;
@@ -62,6 +63,7 @@ cudaError_t launch_prepare_exemplar(const uint8_t* cs, const uint8_t* gs, int ws
 cudaError_t launch_stylize_naive(const StylizeArgs& a, int n_frames, cudaStream_t st, int* launches);
 cudaError_t launch_stylize_tiled(const StylizeArgs& a, int n_frames, cudaStream_t st, int* launches);
 cudaError_t launch_vote(const VoteArgs& a, int n_frames, cudaStream_t st, int* launches);
+cudaError_t launch_vote_wide(const VoteArgs& a, int n_frames, cudaStream_t st, int* launches);
 cudaError_t launch_vote_hist(const VoteArgs& a, int n_frames, cudaStream_t st, int* launches);
 cudaError_t launch_vote_peel(const VoteArgs& a, int n_frames, cudaStream_t st, int* launches);
 

@@ -1,7 +1,9 @@
 // stylize_naive.cu -- one thread per target pixel, Alg. 2 written straight.
 //
-// Kept as the simple baseline kernel (selected with SB_KERNEL=naive) against which the
-// tiled kernel in stylize.cu is measured; both must agree bit for bit with the oracle.
+// Serves what the tiled kernel of stylize.cu does not: L in 10..15 and image sides beyond
+// 32767 (signed coordinates throughout, NearestSeed distances in 64 bits: |s - p| reaches
+// 2h = 2^16 at L = 15).  Also the simple baseline (SB_KERNEL=naive) the tiled kernel is
+// measured against; both agree bit for bit with the oracle.
 #include "sb_kernels.cuh"
 
 namespace sb {
@@ -26,15 +28,15 @@ __global__ void __launch_bounds__(256) stylize_naive_kernel(const __grid_constan
     for (int l = a.L; l >= 1; --l) {
         const uint32_t c_l = level_salt(seed, l);
         const int bx = px >> l, by = py >> l;
-        uint32_t best = 0xFFFFFFFFu;
+        uint64_t best = ~0ull;
         int qx = 0, qy = 0;
         // NearestSeed: x outer, y inner, first strict minimum
         for (int x = -1; x <= 1; ++x)
             for (int y = -1; y <= 1; ++y) {
                 int sx, sy;
                 cell_seed(bx + x, by + y, l, c_l, zj, sx, sy);
-                const int dx = sx - px, dy = sy - py;
-                const uint32_t d = (uint32_t)(dx * dx + dy * dy);
+                const int64_t dx = sx - px, dy = sy - py;
+                const uint64_t d = (uint64_t)(dx * dx + dy * dy);
                 if (d < best) { best = d; qx = sx; qy = sy; }
             }
         qx = min(max(qx, 0), a.wt - 1);  // R8

@@ -610,6 +610,10 @@ static bool launch_tma_r(const VoteArgs& a, int n_frames, cudaStream_t st) {
 }
 
 cudaError_t launch_vote(const VoteArgs& a, int n_frames, cudaStream_t st, int* launches) {
+    // r = 8 or a side beyond 32767: the per-pixel vote of vote_wide.cu (32-bit sums, signed
+    // coordinates); everything else runs on the packed-arithmetic kernels below
+    if (a.r > 7 || a.wt > kPackedMaxDim || a.ht > kPackedMaxDim || a.ws > kPackedMaxDim || a.hs > kPackedMaxDim)
+        return launch_vote_wide(a, n_frames, st, launches);
     // A/B alternatives for r = 1, 2 (measured slower): SB_VOTE=peel the peel vote
     // of vote_peel.cu, SB_VOTE=hist the offset-histogram vote of vote_hist.cu.
     static const int which = [] {

@@ -68,9 +68,9 @@ FAKE = 0x10000  # never dereferenced: validation fails first
     (dict(threshold=float("nan")), "threshold"),
     (dict(threshold=float("inf")), "threshold"),
     (dict(levels=0), "levels"),
-    (dict(levels=13), "levels"),
+    (dict(levels=16), "levels"),
     (dict(blend_radius=-1), "blend_radius"),
-    (dict(blend_radius=8), "blend_radius"),
+    (dict(blend_radius=9), "blend_radius"),
     (dict(guide_channels=1), "guide_channels"),
     (dict(guide_channels=5), "guide_channels"),
     (dict(flags=0x80), "flags"),
@@ -87,7 +87,7 @@ def test_invalid_params(lib, kw, needle):
 
 @pytest.mark.parametrize("args,needle", [
     (dict(cs=0), "cs"), (dict(gs=0), "gs"), (dict(lut=0), "lut"), (dict(gt=0), "gt"), (dict(ct=0), "ct"),
-    (dict(ws=0), "source"), (dict(hs=40000), "source"), (dict(wt=32768), "target"),
+    (dict(ws=0), "source"), (dict(hs=65536), "source"), (dict(wt=65536), "target"),
     (dict(gt=FAKE + 4), "aligned"),
 ])
 def test_invalid_pointers_and_sizes(lib, args, needle):
@@ -98,6 +98,18 @@ def test_invalid_pointers_and_sizes(lib, args, needle):
                         a["ct"], a["coords"], 0, None)
     assert st == _lib.SB_EINVAL
     assert needle in lib.sb_last_error().decode()
+
+
+def test_limits_match_survey_8b(lib):
+    """sides in [1, 65535], L in [1, 15], r in [0, 8] are accepted (validation only:
+    n_frames = 0 launches nothing)."""
+    for kw, dims in ((dict(levels=15), (64, 64, 64, 64)), (dict(blend_radius=8), (64, 64, 64, 64)),
+                     (dict(), (65535, 1, 65535, 1)), (dict(), (1, 65535, 1, 65535))):
+        p = _prm(**kw)
+        ws, hs, wt, ht = dims
+        st = lib.sb_stylize_batch(C.byref(p), 0, None, FAKE, FAKE, ws, hs, FAKE, FAKE, wt, ht, FAKE, FAKE, 0, None)
+        assert st == _lib.SB_OK, (kw, dims, lib.sb_last_error().decode())
+    assert _lib.SB_MAX_LEVELS == 15 and _lib.SB_MAX_RADIUS == 8
 
 
 def test_vote_needs_coords(lib):
@@ -126,7 +138,7 @@ def test_build_lut3_invalid(lib):
     assert lib.sb_build_lut3(FAKE, 4, 4, 0, FAKE, None) == _lib.SB_EINVAL
     assert lib.sb_build_lut3(FAKE, 4, 4, FAKE, 0, None) == _lib.SB_EINVAL
     assert "sb_lut3_workspace_bytes" in lib.sb_last_error().decode()
-    assert lib.sb_build_lut3(FAKE, 4, 40000, FAKE, FAKE, None) == _lib.SB_EINVAL
+    assert lib.sb_build_lut3(FAKE, 4, 65536, FAKE, FAKE, None) == _lib.SB_EINVAL
 
 
 def test_exemplar_copy_abi(lib):

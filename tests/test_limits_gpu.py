@@ -1,0 +1,82 @@
+"""GPU parity at the edges of the SURVEY 8(b) contract that the tiled, packed-coordinate kernels
+do not serve and the per-pixel kernels do (include/styleblit.h: SB_MAX_DIM, SB_MAX_LEVELS,
+SB_MAX_RADIUS): image sides beyond 32767, L = 10..15 and the vote radius r = 8.  Every case is
+compared with the CPU oracle element by element (coords, levels, colours bit-exact)."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1807_03249_b200 as sb
+import synth
+
+pytestmark = pytest.mark.gpu
+NTH = min(16, os.cpu_count() or 1)
+
+
+def _both(cs, gs, gt, t, L, r, C=3, seed=7, with_exemplar=False):
+    csd, gsd, gtd = (torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (cs, gs, gt))
+    lut_d = sb.build_lut(gsd)
+    ex = sb.prepare_exemplar(csd, gsd) if with_exemplar else None
+    prm = sb.Params(threshold=t, levels=L, blend_radius=r, guide_channels=C, seed=seed, exemplar=ex)
+    ct, co, lv = sb.stylize(prm, csd, gsd, lut_d, gtd)
+    torch.cuda.synchronize()
+    lut = oracle.build_lut(gs, nthreads=NTH)
+    assert (lut_d.cpu().numpy().view(np.uint32) == lut).all(), "LUT"
+    oct_, oco, olv = oracle.stylize(oracle.Params(t=t, L=L, C=C, seed=seed), cs, gs, lut, gt, nthreads=NTH)
+    if r > 0:
+        oct_ = oracle.vote(oco, cs, r, nthreads=NTH)
+    g_co = co.cpu().numpy().view(np.uint32)
+    assert (g_co == oco).all(), f"coords: {(g_co != oco).sum()} differ"
+    assert (lv.cpu().numpy() == olv).all(), "levels"
+    g_ct = ct.cpu().numpy()
+    assert (g_ct == oct_).all(), f"colours: {(g_ct != oct_).any(-1).sum()} pixels differ"
+    return olv
+
+
+def _exemplar():
+    cfg = synth.CONFIGS[1]
+    cs, gs = synth.exemplar(cfg)
+    return cs.numpy(), gs.numpy()
+
+
+@pytest.mark.parametrize("L", [10, 13, 15])
+def test_deep_hierarchies(L):
+    """L beyond the tiled kernel's 9: h up to 2^15, NearestSeed distances in 64 bits."""
+    cs, gs = _exemplar()
+    gt = synth.heightfield_normals(203, 150, seed=1).numpy()
+    olv = _both(cs, gs, gt, t=24.0, L=L, r=0)
+    assert olv.max() >= 9, "coarse levels exercised"
+
+
+@pytest.mark.parametrize("r", [7, 8])
+def test_radius_8(r):
+    """r = 8 ((2r+1)^2 * 255 > 2^16: the 32-bit per-pixel vote) next to r = 7 (SWAR kernel)."""
+    cs, gs = _exemplar()
+    gt = synth.heightfield_normals(150, 70, seed=1).numpy()
+    _both(cs, gs, gt, t=32.0, L=3, r=r)
+    _both(cs, gs, gt, t=32.0, L=3, r=r, with_exemplar=True)
+
+
+@pytest.mark.parametrize("wt,ht", [(40000, 3), (5, 33000)])
+def test_wide_targets(wt, ht):
+    """Target sides beyond 32767 (per-pixel stylize and vote with signed coordinates)."""
+    cs, gs = _exemplar()
+    rng = np.random.RandomState(wt + ht)
+    gt = rng.randint(0, 256, (ht, wt, 4)).astype(np.uint8)
+    for r in (0, 2):
+        _both(cs, gs, gt, t=40.0, L=4, r=r)
+
+
+def test_wide_exemplar():
+    """A source wider than 32767 pixels: the LUT build (pixel indices beyond 2^15 rows of
+    16 bits), candidates and votes with signed source coordinates."""
+    rng = np.random.RandomState(5)
+    ws, hs = 33000, 2
+    gs = rng.randint(0, 256, (hs, ws, 4)).astype(np.uint8)
+    cs = rng.randint(0, 256, (hs, ws, 4)).astype(np.uint8)
+    gt = synth.heightfield_normals(130, 20, seed=2).numpy()
+    for r in (0, 2):
+        _both(cs, gs, gt, t=30.0, L=3, r=r)
