@@ -28,22 +28,32 @@ def deps() -> list[str]:
     return sources() + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "styleblit.h")]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(SO) and os.path.getmtime(SO) >= max(os.path.getmtime(d) for d in deps()):
-        return SO
-    tmp = SO + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, "-o", tmp, *sources()]
+SO_CHECKED = os.path.join(HERE, "libstyleblit_checked.so")
+
+
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """nvcc -> libstyleblit.so.  checked=True: libstyleblit_checked.so with -DSB_CHECKED (device
+    bounds checks on every shared-memory slot and global gather/store index, sb_device.cuh),
+    the stand-in for compute-sanitizer memcheck, which this GPU pool does not allow; select it
+    with SB_LIBRARY=.../libstyleblit_checked.so."""
+    so = SO_CHECKED if checked else SO
+    if not force and os.path.exists(so) and os.path.getmtime(so) >= max(os.path.getmtime(d) for d in deps()):
+        return so
+    tmp = so + f".tmp{os.getpid()}"
+    cmd = [NVCC, *NVCC_FLAGS, *(["-DSB_CHECKED"] if checked else []), "-o", tmp, *sources()]
     r = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(HERE, "build.log")
+    log = os.path.join(HERE, "build_checked.log" if checked else "build.log")
     with open(log, "w") as f:
         f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stderr[-4000:]}")
     if verbose:
         print(r.stderr)
-    os.replace(tmp, SO)
-    return SO
+    os.replace(tmp, so)
+    return so
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose=True))
+    import sys
+
+    print(build(force=True, verbose=True, checked="--checked" in sys.argv))

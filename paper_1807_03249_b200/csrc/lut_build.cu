@@ -35,6 +35,7 @@ __global__ void __launch_bounds__(256) lut_sites_kernel(const uint32_t* __restri
         const uint32_t key = valid ? (__ldg(gs + i) & 0xFFFFu) : 0x10000u + lane;
         // lanes holding the same key: the lowest lane has the smallest pixel index
         const unsigned peers = __match_any_sync(0xFFFFFFFFu, key);
+        SB_CHECK(key < 0x10000u + 32u, "site key");
         if (valid && (__ffs(peers) - 1) == lane) atomicMin(site + key, (uint32_t)i);
     }
 }
@@ -134,6 +135,7 @@ __global__ void __launch_bounds__(256) lut_resolve_kernel(const uint2* __restric
         if (d < best_d || (d == best_d && fi < best_i)) { best_d = d; best_i = fi; }
     }
     const uint32_t y = best_i / (uint32_t)ws, x = best_i - y * (uint32_t)ws;
+    SB_CHECK(best_i != 0xFFFFFFFFu, "LUT entry resolved");
     lut[k1 * 256 + k0] = pack_xy((int)x, (int)y);
 }
 

@@ -3,7 +3,27 @@
 // Integer-only formulations of the paper's operations; see DESIGN.md "Kernels".
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
+
+// Bounds checks of the checked build (-DSB_CHECKED, paper_1807_03249_b200/_build.py
+// build(checked=True)): every shared-memory slot and every global gather/store index the
+// kernels compute is tested; a failure prints the site and traps (the launch then fails
+// with an illegal-instruction error).  The pool's compute-sanitizer is closed, so the GPU
+// parity suite runs against this build instead (profiles/r02_checked_suite.txt).  Compiled
+// out of the product build.
+#ifdef SB_CHECKED
+#define SB_CHECK(cond, what)                                                                          \
+    do {                                                                                              \
+        if (!(cond)) {                                                                                \
+            printf("SB_CHECK(%s) failed: %s:%d block (%d,%d,%d) thread %d\n", what, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z, (int)threadIdx.x);               \
+            __trap();                                                                                 \
+        }                                                                                             \
+    } while (0)
+#else
+#define SB_CHECK(cond, what) ((void)0)
+#endif
 
 namespace sb {
 

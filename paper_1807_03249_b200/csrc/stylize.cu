@@ -121,10 +121,12 @@ __device__ __forceinline__ void build_one(const Cells& T, const StylizeArgs& a, 
     cell_seed(g.cx0 + ci, g.cy0 + cj, l, c_l, a.zero_jitter != 0, sx, sy);
     const int qx = min(max(sx, 0), a.wt - 1);
     const int qy = min(max(sy, 0), a.ht - 1);
+    SB_CHECK(qx >= 0 && qx < a.wt && qy >= 0 && qy < a.ht, "table-build G_T[q]");
     const uint32_t u = __ldg(a.lut + (__ldg(gtf + (uint32_t)(qy * a.wt + qx)) & a.key_mask));
     // delta = u* - q packed as dy*65536 + dx: p_packed + delta is the packed candidate s
     const int dpack = ((int)(u >> 16) - qy) * 65536 + ((int)(u & 0xFFFFu) - qx);
     const int idx = g.off + ci * CS + cj;
+    SB_CHECK(ci >= 0 && ci < g.ncx && cj >= 0 && cj < g.ncy && cj < CS && idx >= 0 && idx < 1024, "cell slot");
     const uint32_t Sx = (uint32_t)(32 * (sx - x0)), Sy = (uint32_t)(32 * (sy - y0));
     const uint32_t S2 = Sx * Sx + Sy * Sy + (uint32_t)idx + KOFS;
     const uint32_t X1 = 0u - 64u * Sx;
@@ -163,6 +165,8 @@ __device__ __forceinline__ uint32_t gather_gs(const StylizeArgs& a, const uint32
     asm("min.u16x2 %0, %1, %2;" : "=r"(mn) : "r"(c), "r"(lim));
     *in = mn == c;
     const uint32_t gi = *in ? (PAD ? c : c + (c >> 16) * (uint32_t)(a.ws - 65536)) : 0u;
+    SB_CHECK(PAD ? ((gi & 0xFFFFu) < (uint32_t)a.ws && (gi >> 16) < (uint32_t)a.hs) : gi < (uint32_t)(a.ws * a.hs),
+             "G_S gather");
     const uint32_t* p;
     asm("mad.wide.u32 %0, %1, 4, %2;" : "=l"(p) : "r"(gi), "l"(gs));
     return __ldg(p);
@@ -187,6 +191,7 @@ __device__ __forceinline__ int home_slot(const CellGrid& g, int l, int px, int p
 __device__ __forceinline__ void group_ns(const Cells& T, const CellGrid& g, int l, int x0, int y0, int rx0, int ry,
                                          uint32_t key[4]) {
     const int h0 = home_slot(g, l, x0 + rx0, y0 + ry);
+    SB_CHECK(h0 >= g.off && h0 + 2 * CS + 2 < g.off + g.ncx * CS, "group home slot");
 #pragma unroll
     for (int c = 0; c < 9; ++c) {
         const int slot = h0 + (c / 3) * CS + (c % 3);  // x = c/3 - 1 outer, y = c%3 - 1 inner
@@ -207,6 +212,7 @@ __device__ __forceinline__ void group_ns(const Cells& T, const CellGrid& g, int 
 __device__ __forceinline__ void block_ns(const Cells& T, const CellGrid& g, int l, int x0, int y0, int rx0, int ry0,
                                          uint32_t key[4][4]) {
     const int h0 = home_slot(g, l, x0 + rx0, y0 + ry0);
+    SB_CHECK(h0 >= g.off && h0 + 2 * CS + 2 < g.off + g.ncx * CS, "block home slot");
 #pragma unroll
     for (int c = 0; c < 9; ++c) {
         const int slot = h0 + (c / 3) * CS + (c % 3);
@@ -226,6 +232,7 @@ __device__ __forceinline__ void block_ns(const Cells& T, const CellGrid& g, int 
 
 // delta = u* - q of the winning cell
 __device__ __forceinline__ uint32_t winner_delta(const Cells& T, uint32_t key) {
+    SB_CHECK((key & 1023u) < (uint32_t)MAXCELLS, "winner slot");
     return (uint32_t)T.d[key & 1023u].y;
 }
 
@@ -433,6 +440,7 @@ __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_const
                 uint32_t still = 0, e = 0;
                 if (k < ng) {
                     e = gl[k];
+                    SB_CHECK(k < RPW * NG, "group list");
                     const int grx0 = (int)(e & 31u) * 4;
                     const int ry = row_of((int)((e >> 5) & 7u));
                     const uint32_t m = e >> 8;
@@ -457,6 +465,10 @@ __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_const
                     still = m & ~acc;
                 }
                 const unsigned b = __ballot_sync(0xFFFFFFFFu, still != 0);
+                // in place: entry k is rewritten only at an index <= k; the warp barrier orders
+                // every lane's read of this batch before any lane's write (memory order, not
+                // just convergence: __ballot_sync alone does not promise it)
+                __syncwarp();
                 if (still) gl[nn + __popc(b & lt_mask)] = (uint16_t)((e & 0xFFu) | (still << 8));
                 nn += __popc(b);
             }
@@ -517,6 +529,7 @@ __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_const
             int idx = 0;
             if (k < n) {
                 idx = q[k];
+                SB_CHECK(k < WPX && idx < TP, "pixel queue");
                 const int rx = idx & (TW - 1), ry = idx / TW;
                 const uint32_t cand = direct_candidate(a, gtf, x0 + rx, y0 + ry, l, c_l);
                 const uint32_t gp = sm.coord[cix(idx)];  // G_T while the pixel is rejected
@@ -527,7 +540,8 @@ __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_const
                     rej = true;
                 }
             }
-            const unsigned m = __ballot_sync(0xFFFFFFFFu, rej);  // all reads of this round are done
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, rej);
+            __syncwarp();  // every lane's reads of this round are ordered before the in-place writes
             if (rej) q[nn + __popc(m & lt_mask)] = (uint16_t)idx;  // nn + rank <= k: in place
             nn += __popc(m);
         }
@@ -555,6 +569,8 @@ __global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_const
         const int ry = row_of(j);
         const int64_t o = fpx * frame + (int64_t)((y0 + ry) * wt + (uint32_t)(x0 + rx0));
         const uint4 cv = *reinterpret_cast<const uint4*>(&sm.coord[ry * CROW + rx0]);
+        SB_CHECK(o + nin <= fpx * (frame + 1) && o >= fpx * frame, "output pixel");
+        SB_CHECK((cv.x & 0xFFFFu) < (uint32_t)a.ws && (cv.x >> 16) < (uint32_t)a.hs, "final coordinate");
         if (RAG && nin == 4) {  // a whole group of an unaligned row: the widest stores its address allows
             if (a.coords) st_cs_4w(a.coords + o, cv);
             if (a.level) {

@@ -45,12 +45,14 @@ __global__ void __launch_bounds__(256) stylize_naive_kernel(const __grid_constan
         const int sx = (int)(u & 0xFFFFu) + (px - qx);
         const int sy = (int)(u >> 16) + (py - qy);
         if ((unsigned)sx >= (unsigned)a.ws || (unsigned)sy >= (unsigned)a.hs) continue;  // R9
+        SB_CHECK(qx >= 0 && qx < a.wt && qy >= 0 && qy < a.ht && sx >= 0 && sy >= 0, "naive gathers");
         const uint32_t g = __ldg(gs + (int64_t)sy * a.ws + sx);
         const bool ok = EXT ? guide_ok_ext(gp, g, a.cmask, a.w, a.lmask, a.T2) : guide_d2(gp, g, a.cmask) < a.T2;
         if (ok) { coord = pack_xy(sx, sy); level = l; break; }
     }
     if (level == 0) coord = __ldg(a.lut + (gp & a.key_mask));  // R12
     const int64_t o = fpx * frame + (int64_t)py * a.wt + px;
+    SB_CHECK((coord & 0xFFFFu) < (uint32_t)a.ws && (coord >> 16) < (uint32_t)a.hs, "naive coordinate");
     if (a.coords) a.coords[o] = coord;
     if (a.level) a.level[o] = (uint8_t)level;
     if (a.ct) {

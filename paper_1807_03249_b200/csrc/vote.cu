@@ -127,6 +127,11 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t ws = (uint32_t)a.ws, hs = (uint32_t)a.hs;
     const uint32_t wsl = PAD ? 65536u : ws;  // row stride of the "linear" source index
+    // checked build: a linear source index inside the exemplar (PAD: the packed x | y<<16)
+    auto src_in = [&](uint32_t li) {
+        return PAD ? ((li & 0xFFFFu) < ws && (li >> 16) < hs) : li < ws * hs;
+    };
+    (void)src_in;
 
     const int g = lane;                  // this thread's 4-pixel group column (pixels 4g..4g+3)
     if (fast) {
@@ -203,6 +208,7 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
             for (int k = 0; k < 4; ++k) {
                 o[k] = 0;
                 if ((uni >> k) & 1u) {
+                    SB_CHECK(src_in(cp[k]), "unanimous gather");
                     o[k] = __ldg(cs + cp[k]);
                 } else if ((cx3 >> k) & 1u) {
                     my_mask3 |= 1u << (4 * rr + k);
@@ -246,6 +252,7 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
         const int n = qn;
         for (int j = threadIdx.x; j < n; j += NT) {
             const int idx = queue[j];
+            SB_CHECK(idx >= 0 && idx < TH * TW, "two-run queue");
             const int ry = idx / TW, x = idx - ry * TW;
             uint32_t lo = 0, hi = 0;
 #pragma unroll
@@ -260,6 +267,8 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
                 const uint32_t h2 = c1 < W ? c1 : 0u;                // head of run 2 (or any)
                 const uint32_t* row = &sc[yy][OFF + x - R];
                 const uint32_t shy = (uint32_t)dy * wsl;
+                SB_CHECK(src_in(row[0] - shy + (uint32_t)R) && (c1 == W || src_in(row[h2] - shy - (h2 - (uint32_t)R))),
+                         "two-run gathers");
                 const uint32_t col1 = __ldg(cs + (row[0] - shy + (uint32_t)R));
                 const uint32_t c2 = W - c1;
                 const uint32_t col2 = ldg_if(cs + (row[h2] - shy - (h2 - (uint32_t)R)), c2 != 0);
@@ -272,6 +281,7 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
         const int n3 = qn3;
         for (int j = threadIdx.x; j < n3; j += NT) {
             const int idx = queue[TH * TW - 1 - j];
+            SB_CHECK(idx >= 0 && idx < TH * TW, "run-loop queue");
             const int ry = idx / TW, x = idx - ry * TW;
             uint32_t lo = 0, hi = 0;
 #pragma unroll
@@ -286,6 +296,7 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
                 uint32_t pos = row[0] - shy + (uint32_t)R;
                 while (m) {
                     const uint32_t k = __ffs(m) - 1;
+                    SB_CHECK(src_in(pos), "run gather");
                     const uint32_t c = __ldg(cs + pos);
                     const uint32_t len = k + 1 - start;
                     lo += (c & 0x00FF00FFu) * len;
@@ -294,6 +305,7 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
                     m &= m - 1;
                     pos = row[start] - shy - (start - (uint32_t)R);
                 }
+                SB_CHECK(src_in(pos), "last-run gather");
                 const uint32_t c = __ldg(cs + pos);
                 const uint32_t len = W - start;
                 lo += (c & 0x00FF00FFu) * len;

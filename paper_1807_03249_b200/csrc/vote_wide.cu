@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(WW * WH) vote_wide_kernel(const VoteArgs a) {
             if (w == kOut) continue;
             const int sx = (int)(w & 0xFFFFu) - dx, sy = (int)(w >> 16) - dy;  // src(q) + (p - q)
             if (sx < 0 || sx >= a.ws || sy < 0 || sy >= a.hs) continue;
+            SB_CHECK(sx >= 0 && sx < a.ws && sy >= 0 && sy < a.hs, "wide vote gather");
             const uint32_t c = __ldg(cs + (int64_t)sy * a.ws + sx);
             s0 += c & 0xFFu;
             s1 += (c >> 8) & 0xFFu;

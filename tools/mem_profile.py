@@ -1,13 +1,24 @@
 """Per-SASS-opcode memory cost from `ncu --page source --csv --print-source sass`:
-instructions, L1 tag requests (global), shared wavefronts, L2 theoretical sectors."""
+instructions, L1 tag requests (global), shared wavefronts, L2 theoretical sectors.
+
+usage: ncu -i rep --page source --csv --print-source sass --kernel-name regex:K -c 1 | python tools/mem_profile.py
+
+Only the FIRST kernel section of the input is counted: a report holding several launches of
+the same kernel prints one section per launch, and summing them (the round-1 table did, for two
+stylize launches) doubles every count.  Pass `-c 1` (or `--launch-skip N -c 1`) to pick one."""
 import collections
 import csv
 import sys
 
 agg = collections.defaultdict(lambda: [0.0] * 5)
 hdr = None
+sections = 0
 for row in csv.reader(sys.stdin):
     if row and row[0] == "Address":
+        sections += 1
+        if sections > 1:
+            print("note: more than one kernel section in the input; counting the first only", file=sys.stderr)
+            break
         hdr = {h: i for i, h in enumerate(row)}
         continue
     if hdr is None or len(row) < len(hdr):
