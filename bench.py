@@ -314,6 +314,45 @@ def oracle_section(cid, rad, frames_1t, frames_nt, nth):
                       f"({nth} threads) excluded"}
 
 
+def animation_section(torch, sb, synth, dev):
+    """SURVEY 8(f) #2 as a measured property ("the amount of flickering can be
+    controlled by changing the guidance threshold"): config 2 (1 MP rendered objects, static
+    guide) over 16 frames with per-frame seeds, per threshold t: flicker = mean |C_T^(i+1) -
+    C_T^(i)| over pixels, channels and consecutive frames (8-bit units), for the blit (r = 0)
+    and the vote (r = 2); chunk edges = the fraction of 4-neighbour pixel pairs whose offsets
+    src - p differ (smaller = larger chunks); the share of pixels at level L.  Untimed."""
+    cfg = synth.CONFIGS[2]
+    cs, gs = [t.to(dev) for t in synth.exemplar(cfg, device=dev)]
+    lut = sb.build_lut(gs)
+    gt1 = synth.target(2, device=dev)
+    n = 16
+    frames = gt1.unsqueeze(0).expand(n, *gt1.shape).contiguous()
+    H, W = gt1.shape[:2]
+    xs = torch.arange(W, device=dev, dtype=torch.int64).view(1, 1, W)
+    ys = torch.arange(H, device=dev, dtype=torch.int64).view(1, H, 1)
+    rows = []
+    for t in (4.0, 8.0, 12.0, 24.0, 48.0):
+        row = {"t": t}
+        for r in (0, 2):
+            prm = sb.Params(threshold=t, levels=cfg["L"], blend_radius=r, guide_channels=cfg["C"], seed=1)
+            ct, co, lv = sb.stylize_batch(prm, cs, gs, lut, frames)  # seeds 1 .. 16
+            d = (ct[1:].to(torch.int16) - ct[:-1].to(torch.int16)).abs().float().mean().item()
+            row[f"flicker_r{r}"] = round(d, 3)
+            if r == 0:
+                c = co.to(torch.int64) & 0xFFFFFFFF
+                off = ((c & 0xFFFF) - xs) * 65536 + ((c >> 16) - ys)
+                e = ((off[:, :, 1:] != off[:, :, :-1]).sum() + (off[:, 1:] != off[:, :-1]).sum()).item()
+                row["chunk_edge_fraction"] = round(e / (n * (H * (W - 1) + (H - 1) * W)), 4)
+                row["share_level_L"] = round((lv == cfg["L"]).float().mean().item(), 4)
+        rows.append(row)
+    prm = sb.Params(threshold=12.0, levels=cfg["L"], guide_channels=cfg["C"], seed=1)
+    same = sb.stylize_batch(prm, cs, gs, lut, frames, frame_seeds=[5] * n)[0]
+    still = (same[1:].to(torch.int16) - same[:-1].to(torch.int16)).abs().float().mean().item()
+    return {"workload": "cfg2 1 MP static guide, 16 frames, seeds 1..16, L=5, C=3", "rows": rows,
+            "flicker_fixed_seed_t12": round(still, 3),
+            "note": "flicker grows with t and chunks grow (fewer edges); a fixed seed gives identical frames"}
+
+
 def config_sections(args, torch, sb, synth, dev, stream, hbm, with_oracle):
     """BASELINE.json configs other than the headline, each with its own value, roofline, level
     histogram and the oracle timed beside it; plus the single-frame 4K latency and a ragged
@@ -333,6 +372,7 @@ def config_sections(args, torch, sb, synth, dev, stream, hbm, with_oracle):
     rag = gpu_section(torch, sb, synth, dev, stream, hbm, 5, args.frames, 0, st, wu, wt=3838, ht=2160)
     rag["note"] = "cfg5 workload at a width not divisible by 4 (3838): the tiled kernel's per-pixel row I/O"
     secs["ragged_3838x2160"] = rag
+    secs["animation_flicker_vs_t"] = animation_section(torch, sb, synth, dev)
     return secs
 
 
