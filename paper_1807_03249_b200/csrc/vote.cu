@@ -35,6 +35,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <type_traits>
 #include <map>
 #include <mutex>
 
@@ -99,7 +100,10 @@ struct VoteShared {
     static constexpr int SH = VoteGeom<R>::SH;
     uint8_t seg[SH][NG];        // nibble: which of the group's 4 row segments are one chunk
     uint8_t seg3[SH][NG];       // nibble: which of them have three or more runs
-    uint32_t hl[SH][6];         // row link bits: bit x+32 <=> position x+1 continues x
+    uint8_t vseg[SH][NG];       // nibble: which of the group's 4 columns continue into the next row
+    // the 2r link bits of the window row centred at each staged position (bit i: window position
+    // i+1 continues i)
+    std::conditional_t<(2 * R <= 8), uint8_t, uint16_t> wl[SH][TW];
     __align__(16) uint32_t outc[TH][TW];
     uint16_t queue[TH * TW];    // two-run pixels from the front, others from the back
     int qn, qn3;
@@ -117,7 +121,8 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
     constexpr int SH = VoteGeom<R>::SH, KR = VoteGeom<R>::KR, OFF = VoteGeom<R>::OFF, SWP = VoteGeom<R>::SWP;
     auto& seg = S.seg;
     auto& seg3 = S.seg3;
-    auto& hl = S.hl;
+    auto& vseg = S.vseg;
+    auto& wl = S.wl;
     auto& outc = S.outc;
     auto& queue = S.queue;
     int& qn = S.qn;
@@ -170,14 +175,14 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
 #pragma unroll
                 for (int k = 0; k < 4; ++k) nib3 |= (uint32_t)(__popc(~(link >> k) & win) >= 2) << k;
                 seg3[yy][gg] = (uint8_t)nib3;
-                // assemble the row's link words (a warp holds one staged row: lane == group)
-                uint32_t wv = ((link >> R) & 0xFu) << (4 * (gg & 7));
-                wv |= __shfl_xor_sync(0xFFFFFFFFu, wv, 1);
-                wv |= __shfl_xor_sync(0xFFFFFFFFu, wv, 2);
-                wv |= __shfl_xor_sync(0xFFFFFFFFu, wv, 4);
-                if ((gg & 7) == 0) hl[yy][1 + (gg >> 3)] = wv;
-                if (gg == 0) hl[yy][0] = (link & ((1u << R) - 1u)) << (32 - R);
-                if (gg == NG - 1) hl[yy][5] = (link >> (R + 4)) & ((1u << (R - 1)) - 1u);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) wl[yy][4 * gg + k] = (link >> k) & win;
+                if (yy + 1 < SH) {  // vertical continuity of the group's 4 columns into row yy+1
+                    const uint4 d = *reinterpret_cast<const uint4*>(&sc[yy + 1][OFF + 4 * gg]);
+                    const uint32_t* c = u + 4 * KR;  // this row's columns 4gg .. 4gg+3
+                    vseg[yy][gg] = (uint8_t)((uint32_t)(d.x == c[0] + wsl) | ((uint32_t)(d.y == c[1] + wsl) << 1) |
+                                             ((uint32_t)(d.z == c[2] + wsl) << 2) | ((uint32_t)(d.w == c[3] + wsl) << 3));
+                }
             }
             __syncthreads();
         }
@@ -191,17 +196,14 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
             if (y0 + ry >= a.row_end || x0 + 4 * g >= a.wt) continue;
             const uint4 c4 = *reinterpret_cast<const uint4*>(&sc[ry + R][OFF + 4 * g]);
             const uint32_t cp[4] = {c4.x, c4.y, c4.z, c4.w};
+            // unanimous: every window row is one run and the 2r+1 rows continue each other
+            // vertically (the centre column)
             uint32_t uni = 0xFu, cx3 = 0;
 #pragma unroll
             for (int j = -R; j <= R; ++j) {
-                uint32_t m = seg[ry + R + j][g];
+                uni &= (R > 0) ? (uint32_t)seg[ry + R + j][g] : 0xFu;
+                if (j < R) uni &= (uint32_t)vseg[ry + R + j][g];
                 cx3 |= seg3[ry + R + j][g];
-                const uint4 v4 = *reinterpret_cast<const uint4*>(&sc[ry + R + j][OFF + 4 * g]);
-                const uint32_t vv[4] = {v4.x, v4.y, v4.z, v4.w};
-                const uint32_t sh = (uint32_t)j * wsl;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) m &= ~((uint32_t)(vv[k] != cp[k] + sh) << k);
-                uni &= (R > 0) ? m : 0xFu;
             }
             uint32_t o[4];
 #pragma unroll
@@ -258,8 +260,7 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
 #pragma unroll
             for (int dy = -R; dy <= R; ++dy) {
                 const int yy = ry + R + dy;
-                const uint32_t b = (uint32_t)(x - R + 32);
-                const uint32_t bits = __funnelshift_r(hl[yy][b >> 5], hl[yy][(b >> 5) + 1], b & 31u);
+                const uint32_t bits = wl[yy][x];
                 // length of run 1 = position of the first run end + 1 (W if none): with t the
                 // link bits, t ^ (t + 1) has exactly c1 low bits set
                 const uint32_t t = bits & ((1u << (2 * R)) - 1u);
@@ -287,8 +288,7 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
 #pragma unroll
             for (int dy = -R; dy <= R; ++dy) {
                 const int yy = ry + R + dy;
-                const uint32_t b = (uint32_t)(x - R + 32);
-                const uint32_t bits = __funnelshift_r(hl[yy][b >> 5], hl[yy][(b >> 5) + 1], b & 31u);
+                const uint32_t bits = wl[yy][x];
                 uint32_t m = ~bits & ((1u << (2 * R)) - 1u);  // bit i: a run ends at window position i
                 const uint32_t* row = &sc[yy][OFF + x - R];
                 const uint32_t shy = (uint32_t)dy * wsl;
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteAr
 }
 
 
-// ---- TMA-fed persistent kernel (rows of 16-byte multiple strides, i.e. wt % 4 == 0) ----
+// ---- TMA-fed persistent kernel (r <= 4; rows of 16-byte multiple strides, i.e. wt % 4 == 0) ----
 // One CTA per resident slot loops over tiles (frame-major); the staged coordinates of tile k+1
 // are fetched by the Tensor Memory Accelerator (one 3-D box [frame][SH rows][SWP columns],
 // zero-filled outside the tensor) into the other of two shared buffers while tile k is voted,
@@ -544,13 +544,13 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2))
     }
 }
 
-// Shared memory carved out of the unified L1: the vote's C_S gathers live in L1, and a 60 %
-// carve-out (fewer resident CTAs, more L1) measured ~4 % faster than the default on B200
-// (profiles/carveout_sweep.sh).  SB_VOTE_CARVEOUT (percent, -1 = driver default) overrides.
+// Shared-memory carve-out preference of the grid-per-tile vote: the driver's default (-1) since
+// round 2 (a 60 % carve-out was ~4 % faster for round 1's smaller shared footprint and is ~2.5 %
+// slower for the current one).  SB_VOTE_CARVEOUT (percent) overrides.
 static int vote_carveout() {
     static const int pct = [] {
         const char* e = getenv("SB_VOTE_CARVEOUT");
-        return e ? atoi(e) : 60;
+        return e ? atoi(e) : -1;
     }();
     return pct;
 }
@@ -650,9 +650,7 @@ cudaError_t launch_vote(const VoteArgs& a, int n_frames, cudaStream_t st, int* l
             case 2: done = launch_tma_r<2>(a, n_frames, st); break;
             case 3: done = launch_tma_r<3>(a, n_frames, st); break;
             case 4: done = launch_tma_r<4>(a, n_frames, st); break;
-            case 5: done = launch_tma_r<5>(a, n_frames, st); break;
-            case 6: done = launch_tma_r<6>(a, n_frames, st); break;
-            case 7: break;  // two r = 7 buffers exceed the 48 KB of static shared memory
+            case 5: case 6: case 7: break;  // two staging buffers exceed 48 KB of static shared memory
             default: return cudaErrorInvalidValue;
         }
         if (done) {
