@@ -106,7 +106,8 @@ struct VoteShared {
     std::conditional_t<(2 * R <= 8), uint8_t, uint16_t> wl[SH][TW];
     __align__(16) uint32_t outc[TH][TW];
     uint16_t queue[TH * TW];    // two-run pixels from the front, others from the back
-    int qn, qn3;
+    uint16_t qe[2 * R * (TW + TH) + 1];  // fast tiles at the frame edge: pixels within r of it
+    int qn, qn3, qne;
 };
 
 // The vote of one tile whose coordinates (tile + r halo, kOutside outside the target) are
@@ -127,6 +128,11 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
     auto& queue = S.queue;
     int& qn = S.qn;
     int& qn3 = S.qn3;
+    int& qne = S.qne;
+    auto& qe = S.qe;
+    // a fast tile at the frame edge: its pixels within r of the edge (windows clipped by the
+    // target) take the per-position path; every other pixel the fast path
+    const bool edge_tile = x0 - R < 0 || x0 + TW + R > a.wt || y0 - R < 0 || y0 + TH + R > a.ht;
     const int64_t fpx = (int64_t)a.wt * a.ht;
     const uint32_t* __restrict__ cs = reinterpret_cast<const uint32_t*>(PAD ? a.cs_pad : a.cs);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -188,8 +194,8 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
         }
         // ---- 2. per pixel: unanimous window -> blit; else queue it, apart if a window row has
         //      three or more runs
-        int my_n = 0, my_n3 = 0;
-        uint32_t my_mask = 0, my_mask3 = 0;  // bit 4*rr + k: queued
+        int my_n = 0, my_n3 = 0, my_ne = 0;
+        uint32_t my_mask = 0, my_mask3 = 0, my_maske = 0;  // bit 4*rr + k: queued
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
             const int ry = warp + 8 * rr;
@@ -209,7 +215,13 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 o[k] = 0;
-                if ((uni >> k) & 1u) {
+                const int gx = x0 + 4 * g + k, gy = y0 + ry;
+                if (edge_tile && (gx >= a.wt || gx < R || gx >= a.wt - R || gy < R || gy >= a.ht - R)) {
+                    if (gx < a.wt) {  // pixels past a ragged row end are neither computed nor written
+                        my_maske |= 1u << (4 * rr + k);
+                        ++my_ne;
+                    }
+                } else if ((uni >> k) & 1u) {
                     SB_CHECK(src_in(cp[k]), "unanimous gather");
                     o[k] = __ldg(cs + cp[k]);
                 } else if ((cx3 >> k) & 1u) {
@@ -239,6 +251,11 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
             }
             base = __shfl_sync(0xFFFFFFFFu, base, 31) + incl - my_n;
             base3 = __shfl_sync(0xFFFFFFFFu, base3, 31) + incl3 - my_n3;
+            if (edge_tile && my_ne) {  // few pixels, only in frame-edge tiles: one atomic per thread
+                int be = atomicAdd(&qne, my_ne);
+                for (int b = 0; b < 8; ++b)
+                    if (my_maske & (1u << b)) qe[be++] = (uint16_t)((warp + 8 * (b >> 2)) * TW + 4 * g + (b & 3));
+            }
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
                 const uint16_t id = (uint16_t)((warp + 8 * (b >> 2)) * TW + 4 * g + (b & 3));
@@ -313,6 +330,31 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
             }
             outc[ry][x] = finish_const<W * W>(lo, hi);
         }
+        // ---- 3c. frame-edge pixels of a fast tile: the general per-position path (clipped window)
+        if (edge_tile) {
+            const int ne = qne;
+            for (int j = threadIdx.x; j < ne; j += NT) {
+                const int idx = qe[j];
+                SB_CHECK(idx >= 0 && idx < TH * TW, "edge queue");
+                const int ry = idx / TW, x = idx - ry * TW;
+                uint32_t lo = 0, hi = 0, cnt = 0;
+#pragma unroll
+                for (int dy = -R; dy <= R; ++dy) {
+#pragma unroll
+                    for (int dx = -R; dx <= R; ++dx) {
+                        // staged values are linear source indices here (the conversion pass ran;
+                        // kOutside was converted too, so clip by position)
+                        const int qx = x0 + x + dx, qy = y0 + ry + dy;
+                        const bool in = qx >= 0 && qx < a.wt && qy >= 0 && qy < a.ht;
+                        const uint32_t li = sc[ry + R + dy][OFF + x + dx] - (uint32_t)dx - (uint32_t)dy * wsl;
+                        SB_CHECK(!in || src_in(li), "edge gather");
+                        const uint32_t c = ldg_if(cs + (in ? li : 0u), in);
+                        if (in) { swar_add(c, lo, hi); ++cnt; }
+                    }
+                }
+                outc[ry][x] = finish(lo, hi, cnt);
+            }
+        }
     } else {
         // ---- border tile: every pixel takes the general path
         const int ntile = TH * TW;
@@ -371,7 +413,7 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteAr
     const int64_t fpx = (int64_t)a.wt * a.ht;
     const uint32_t* __restrict__ cf = a.coords + fpx * blockIdx.y;
     const uint32_t ws = (uint32_t)a.ws, hs = (uint32_t)a.hs;
-    if (threadIdx.x == 0) S.qn = S.qn3 = 0;
+    if (threadIdx.x == 0) S.qn = S.qn3 = S.qne = 0;
     // ---- stage coords (tile + halo), outside the target -> kOutside; test the fast-tile margin
     bool fast_mine = true;
     auto stage = [&](int yy, int x, uint32_t v, bool in) {  // x: tile column (-R .. TW-1+R)
@@ -379,8 +421,7 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteAr
             const uint32_t sx = v & 0xFFFFu, sy = v >> 16;
             fast_mine &= (sx >= (uint32_t)R) & (sx + (uint32_t)R < ws) & (sy >= (uint32_t)R) & (sy + (uint32_t)R < hs);
         } else {
-            v = kOutside;
-            fast_mine = false;
+            v = kOutside;  // outside the target: only the frame-edge pixels' windows see it
         }
         sc[yy][OFF + x] = v;
     };
@@ -506,7 +547,7 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2))
         if (tid == 0) {
             const int tn = t + gridDim.x;  // the next tile into the other buffer (free since the last barrier)
             if (tn < n_tiles) fetch(tn, b ? (void*)sc0 : (void*)sc1, &mbar[b ^ 1]);
-            S.qn = S.qn3 = 0;
+            S.qn = S.qn3 = S.qne = 0;
         }
         int x0, y0, f;
         origin(t, x0, y0, f);
@@ -524,16 +565,18 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2))
             bool out = false;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
+                bool in = true;
                 if (edge) {
                     const int gx = x0 - OFF + 4 * c4 + j, gy = y0 - R + yy;
                     if (gx < 0 || gx >= a.wt || gy < 0 || gy >= a.ht) {
                         vv[j] = kOutside;
                         out = true;
+                        in = false;
                     }
                 }
                 const uint32_t sx = vv[j] & 0xFFFFu, sy = vv[j] >> 16;
-                m |= (uint32_t)((sx < (uint32_t)R) | (sx + (uint32_t)R >= ws) | (sy < (uint32_t)R) |
-                                (sy + (uint32_t)R >= hs));
+                m |= (uint32_t)(in & ((sx < (uint32_t)R) | (sx + (uint32_t)R >= ws) | (sy < (uint32_t)R) |
+                                      (sy + (uint32_t)R >= hs)));
             }
             fast_mine &= (m == 0);
             if (out) *reinterpret_cast<uint4*>(&sc[yy][4 * c4]) = make_uint4(vv[0], vv[1], vv[2], vv[3]);
