@@ -309,7 +309,7 @@ sb_status sb_vote(const uint32_t* coords, int32_t n_frames, int32_t wt, int32_t 
     const int64_t fpx = (int64_t)wt * ht;
     for (int f0 = 0; f0 < n_frames; f0 += 65535) {
         const int nf = (n_frames - f0) < 65535 ? (n_frames - f0) : 65535;
-        sb::VoteArgs v;
+        sb::VoteArgs v{};
         v.coords = coords + fpx * f0; v.cs = cs; v.ws = ws; v.hs = hs; v.wt = wt; v.ht = ht; v.r = r;
         v.cs_pad = exemplar ? exemplar + (size_t)hs * ((size_t)1 << 18) : nullptr;
         v.ct = ct + 4 * fpx * f0; v.row_begin = row_begin; v.row_end = row_end;
