@@ -46,7 +46,9 @@ namespace sb {
 namespace {
 constexpr int TW = 128, TH = 16, NT = 256;
 constexpr int NG = TW / 4;                   // 4-pixel groups per row
-constexpr uint32_t kOutside = 0xFFFFFFFFu;   // window position outside the target
+// window position outside the target: fields 0xC000 stay >= 0xC000 - 8 > 32767 after any window
+// offset, so the packed in-source test rejects it by itself (and it never links with a coordinate)
+constexpr uint32_t kOutside = 0xC000C000u;
 
 __device__ __forceinline__ uint32_t finish(uint32_t lo, uint32_t hi, uint32_t n) {
     if (n <= 1) return (lo & 0x00FF00FFu) | ((hi & 0x00FF00FFu) << 8);
@@ -358,6 +360,7 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
     } else {
         // ---- border tile: every pixel takes the general path
         const int ntile = TH * TW;
+        const uint32_t lim = ((hs - 1u) << 16) | (ws - 1u);
         for (int idx = threadIdx.x; idx < ntile; idx += NT) {
             const int ry = idx / TW, x = idx - ry * TW;
             const int gx = x0 + x;
@@ -370,7 +373,10 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
                 for (int dx = -R; dx <= R; ++dx) {
                     const uint32_t w = sc[ry + R + dy][OFF + x + dx];
                     const uint32_t pos = w - (uint32_t)dx - sh;
-                    const bool in = (w != kOutside) & ((pos & 0xFFFFu) < ws) & ((pos >> 16) < hs);
+                    // inside the source (and the target: see kOutside): one packed 16-bit min
+                    uint32_t mn;
+                    asm("min.u16x2 %0, %1, %2;" : "=r"(mn) : "r"(pos), "r"(lim));
+                    const bool in = mn == pos;
                     const uint32_t c = __ldg(cs + (in ? (PAD ? pos : (pos >> 16) * ws + (pos & 0xFFFFu)) : 0u));
                     if (in) { swar_add(c, lo, hi); ++cnt; }
                 }
