@@ -335,6 +335,7 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
         // ---- 3c. frame-edge pixels of a fast tile: the general per-position path (clipped window)
         if (edge_tile) {
             const int ne = qne;
+            const uint32_t lim = ((hs - 1u) << 16) | (ws - 1u);
             for (int j = threadIdx.x; j < ne; j += NT) {
                 const int idx = qe[j];
                 SB_CHECK(idx >= 0 && idx < TH * TW, "edge queue");
@@ -344,11 +345,16 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
                 for (int dy = -R; dy <= R; ++dy) {
 #pragma unroll
                     for (int dx = -R; dx <= R; ++dx) {
-                        // staged values are linear source indices here (the conversion pass ran;
-                        // kOutside was converted too, so clip by position)
-                        const int qx = x0 + x + dx, qy = y0 + ry + dy;
-                        const bool in = qx >= 0 && qx < a.wt && qy >= 0 && qy < a.ht;
                         const uint32_t li = sc[ry + R + dy][OFF + x + dx] - (uint32_t)dx - (uint32_t)dy * wsl;
+                        bool in;
+                        if (PAD) {  // packed: kOutside fails the in-source test (sources of a fast tile are in)
+                            uint32_t mn;
+                            asm("min.u16x2 %0, %1, %2;" : "=r"(mn) : "r"(li), "r"(lim));
+                            in = mn == li;
+                        } else {  // linear indices (the conversion pass ran, kOutside too): clip by position
+                            const int qx = x0 + x + dx, qy = y0 + ry + dy;
+                            in = qx >= 0 && qx < a.wt && qy >= 0 && qy < a.ht;
+                        }
                         SB_CHECK(!in || src_in(li), "edge gather");
                         const uint32_t c = ldg_if(cs + (in ? li : 0u), in);
                         if (in) { swar_add(c, lo, hi); ++cnt; }
