@@ -437,6 +437,12 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteAr
         }
         sc[yy][OFF + x] = v;
     };
+    // the fast-tile margin as packed 16-bit bounds: (R, R) .. (ws-1-R, hs-1-R)
+    // (an exemplar no wider or taller than 2R has no such position)
+    const uint32_t mlo = ((uint32_t)R << 16) | (uint32_t)R;
+    const bool room = ws > 2u * R && hs > 2u * R;
+    const uint32_t mhi = room ? ((hs - 1u - (uint32_t)R) << 16) | (ws - 1u - (uint32_t)R) : 0u;
+    fast_mine &= room;
     if ((a.wt & 3) == 0) {
         // centre columns: one 16-byte load per 4 pixels
         for (int i = threadIdx.x; i < SH * NG; i += NT) {
@@ -445,15 +451,16 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteAr
             const bool rowin = gy >= 0 && gy < a.ht;
             if (rowin && gx + 3 < a.wt) {
                 const uint4 v = *reinterpret_cast<const uint4*>(cf + (int64_t)gy * a.wt + gx);
-                uint32_t m = 0;
                 const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+                bool ok = true;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint32_t sx = vv[k] & 0xFFFFu, sy = vv[k] >> 16;
-                    m |= (uint32_t)((sx < (uint32_t)R) | (sx + (uint32_t)R >= ws) | (sy < (uint32_t)R) |
-                                    (sy + (uint32_t)R >= hs));
+                for (int k = 0; k < 4; ++k) {  // R <= x < ws - R and R <= y < hs - R, both fields at once
+                    uint32_t lo, hi;
+                    asm("max.u16x2 %0, %1, %2;" : "=r"(lo) : "r"(vv[k]), "r"(mlo));
+                    asm("min.u16x2 %0, %1, %2;" : "=r"(hi) : "r"(vv[k]), "r"(mhi));
+                    ok &= (lo == vv[k]) & (hi == vv[k]);
                 }
-                fast_mine &= (m == 0);
+                fast_mine &= ok;
                 *reinterpret_cast<uint4*>(&sc[yy][OFF + 4 * gg]) = v;
             } else {
 #pragma unroll
