@@ -237,22 +237,32 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
             *reinterpret_cast<uint4*>(&outc[ry][4 * g]) = make_uint4(o[0], o[1], o[2], o[3]);
         }
         {
-            int incl = my_n, incl3 = my_n3;
+            // queue slots row by row: the warp's row-ry pixels, then its row-ry+8 pixels (the
+            // counts of the two rows scan together in the 16-bit halves of one word), so the
+            // lanes of a dense pass mostly read one staged row (rows 8 apart share banks)
+            const uint32_t c2 = (uint32_t)__popc(my_mask & 0xFu) | ((uint32_t)__popc(my_mask >> 4) << 16);
+            const uint32_t c3 = (uint32_t)__popc(my_mask3 & 0xFu) | ((uint32_t)__popc(my_mask3 >> 4) << 16);
+            uint32_t incl = c2, incl3 = c3;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                const int v3 = __shfl_up_sync(0xFFFFFFFFu, incl3, o);
+                const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                const uint32_t v3 = __shfl_up_sync(0xFFFFFFFFu, incl3, o);
                 if (lane >= o) { incl += v; incl3 += v3; }
             }
-            const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-            const int total3 = __shfl_sync(0xFFFFFFFFu, incl3, 31);
+            const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+            const uint32_t total3 = __shfl_sync(0xFFFFFFFFu, incl3, 31);
+            const int t0 = (int)(total & 0xFFFFu), t1 = (int)(total >> 16);
+            const int u0 = (int)(total3 & 0xFFFFu), u1 = (int)(total3 >> 16);
             int base = 0, base3 = 0;
             if (lane == 31) {
-                if (total) base = atomicAdd(&qn, total);
-                if (total3) base3 = atomicAdd(&qn3, total3);
+                if (t0 + t1) base = atomicAdd(&qn, t0 + t1);
+                if (u0 + u1) base3 = atomicAdd(&qn3, u0 + u1);
             }
-            base = __shfl_sync(0xFFFFFFFFu, base, 31) + incl - my_n;
-            base3 = __shfl_sync(0xFFFFFFFFu, base3, 31) + incl3 - my_n3;
+            base = __shfl_sync(0xFFFFFFFFu, base, 31);
+            base3 = __shfl_sync(0xFFFFFFFFu, base3, 31);
+            const uint32_t ex = incl - c2, ex3 = incl3 - c3;  // exclusive prefixes, both halves
+            int b2[2] = {base + (int)(ex & 0xFFFFu), base + t0 + (int)(ex >> 16)};
+            int b3[2] = {base3 + (int)(ex3 & 0xFFFFu), base3 + u0 + (int)(ex3 >> 16)};
             if (edge_tile && my_ne) {  // few pixels, only in frame-edge tiles: one atomic per thread
                 int be = atomicAdd(&qne, my_ne);
                 for (int b = 0; b < 8; ++b)
@@ -261,8 +271,8 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
                 const uint16_t id = (uint16_t)((warp + 8 * (b >> 2)) * TW + 4 * g + (b & 3));
-                if (my_mask & (1u << b)) queue[base++] = id;
-                if (my_mask3 & (1u << b)) queue[TH * TW - 1 - base3++] = id;
+                if (my_mask & (1u << b)) queue[b2[b >> 2]++] = id;
+                if (my_mask3 & (1u << b)) queue[TH * TW - 1 - b3[b >> 2]++] = id;
             }
         }
         __syncthreads();
