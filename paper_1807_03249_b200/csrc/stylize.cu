@@ -1,7 +1,7 @@
 // stylize.cu -- tiled Alg. 2 "ParallelStyleBlit" for sm_100a.
 //
 // One CTA = one 128 x 16 pixel tile of one frame (grid = tiles_x x tiles_y x frames), 128
-// threads, 8 CTAs per SM (small CTAs: a CTA waiting at its table-build barrier idles only 4
+// threads, 9 CTAs per SM (56 registers; 8 for ragged widths) (small CTAs: a CTA waiting at its table-build barrier idles only 4
 // warps); warp w owns tile rows 4w .. 4w+3 and a thread owns 4 consecutive pixels of each
 // (uint4 I/O), i.e. a 4-aligned 4 x 4 pixel block.  Per tile and level l the seed cells that
 // any tile pixel can reach (its 3x3 neighbourhood) are materialised in
@@ -307,7 +307,7 @@ __device__ __forceinline__ uint32_t direct_candidate(const StylizeArgs& a, const
 // has 1..3 pixels, so G_T is read and the outputs are written pixel by pixel there (pixels past
 // the row end are computed on G_T = 0 and never written).
 template <bool EXT, bool LVL, int LT, bool PAD, bool NOCT = false, bool RAG = false>
-__global__ void __launch_bounds__(NT, 8) stylize_tiled_kernel(const __grid_constant__ StylizeArgs a) {
+__global__ void __launch_bounds__(NT, RAG ? 8 : 9) stylize_tiled_kernel(const __grid_constant__ StylizeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
     const int L = LT > 0 ? LT : a.L;
