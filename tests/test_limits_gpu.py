@@ -80,3 +80,24 @@ def test_wide_exemplar():
     gt = synth.heightfield_normals(130, 20, seed=2).numpy()
     for r in (0, 2):
         _both(cs, gs, gt, t=30.0, L=3, r=r)
+
+
+@pytest.mark.parametrize("L,r,wt,ht", [(15, 8, 96, 40), (12, 2, 40000, 2)])
+def test_host_pipeline_at_the_limits(L, r, wt, ht):
+    """sb_stylize_batch_host (host frames in and out) on the per-pixel kernels: L = 15 with r = 8,
+    and a 40000-wide batch -- equal to the device batch, which equals the oracle (above)."""
+    cs, gs = _exemplar()
+    rng = np.random.RandomState(L + r)
+    gt = rng.randint(0, 256, (3, ht, wt, 4)).astype(np.uint8)
+    csd, gsd = torch.from_numpy(cs).cuda(), torch.from_numpy(gs).cuda()
+    lut = sb.build_lut(gsd)
+    prm = sb.Params(threshold=40.0, levels=L, blend_radius=r, guide_channels=3, seed=3)
+    dev_ct, _, _ = sb.stylize_batch(prm, csd, gsd, lut, torch.from_numpy(gt).cuda(), want_level=False)
+    gt_h = torch.from_numpy(gt).pin_memory()
+    ct_h = torch.empty_like(gt_h).pin_memory()
+    sb.stylize_batch_host(prm, csd, gsd, lut, gt_h, ct_h)
+    assert torch.equal(ct_h, dev_ct.cpu())
+    o = oracle.stylize(oracle.Params(t=40.0, L=L, C=3, seed=3 + 1), cs, gs, oracle.build_lut(gs, nthreads=NTH),
+                       gt[1], nthreads=NTH)
+    want = oracle.vote(o[1], cs, r, nthreads=NTH) if r > 0 else o[0]
+    assert (ct_h[1].numpy() == want).all()

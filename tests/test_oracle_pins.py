@@ -58,9 +58,9 @@ def test_seed_point_lies_in_its_cell():
     with j in [0,1)^2 the seed of cell b stays inside cell b."""
     rng = np.random.RandomState(0)
     for _ in range(2000):
-        l = int(rng.randint(1, 8))
+        l = int(rng.randint(1, 16))  # the whole 8(b) range of L (h up to 2^15)
         h = 1 << l
-        px, py = (int(v) for v in rng.randint(-3000, 3000, 2))
+        px, py = (int(v) for v in rng.randint(-70000, 70000, 2))
         sx, sy = oracle.seed_point(px, py, l, SEED)
         bx, by = px // h, py // h  # python // is floor division
         assert bx * h <= sx < (bx + 1) * h and by * h <= sy < (by + 1) * h
@@ -92,6 +92,17 @@ def test_nearest_seed_zero_jitter_closed_form():
                 ex = (px // h) * h + (h if px % h > h / 2 else 0)
                 ey = (py // h) * h + (h if py % h > h / 2 else 0)
                 assert oracle.nearest_seed(px, py, l, SEED, zero_jitter=True) == (ex, ey), (l, px, py)
+    # deep levels (h up to 2^15, image sides up to 65535): sampled points, the exact half-way
+    # points and their neighbours included
+    rng = np.random.RandomState(7)
+    for l in (10, 13, 15):
+        h = 1 << l
+        pts = [int(v) for v in rng.randint(0, 65535, 40)] + [h // 2 - 1, h // 2, h // 2 + 1, h - 1, h, 65534]
+        for px in pts:
+            py = int(rng.randint(0, 65535))
+            ex = (px // h) * h + (h if px % h > h / 2 else 0)
+            ey = (py // h) * h + (h if py % h > h / 2 else 0)
+            assert oracle.nearest_seed(px, py, l, SEED, zero_jitter=True) == (ex, ey), (l, px, py)
 
 
 def _cands(px, py, l, seed):
@@ -111,9 +122,9 @@ def test_nearest_seed_is_first_minimum_in_loop_order():
     rng = np.random.RandomState(1)
     n_ties = n_checked = n_far = 0
     for _ in range(3000):
-        l = int(rng.randint(1, 6))
+        l = int(rng.randint(1, 6)) if _ % 10 else int(rng.randint(6, 16))  # every 10th: a deep level
         h = 1 << l
-        px, py = (int(v) for v in rng.randint(0, 500, 2))
+        px, py = (int(v) for v in rng.randint(0, 500 if l < 6 else 65535, 2))
         q = oracle.nearest_seed(px, py, l, SEED)
         c = _cands(px, py, l, SEED)
         dmin = min(d for d, _, _ in c)
