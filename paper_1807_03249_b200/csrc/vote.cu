@@ -425,7 +425,7 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
 
 // The grid-per-tile kernel: coordinates staged with 16-byte loads (any width).
 template <int R, bool PAD>
-__global__ void __launch_bounds__(NT, (R <= 3 ? 6 : 2)) vote_kernel(const VoteArgs a) {
+__global__ void __launch_bounds__(NT, (R <= 3 ? 6 : (R == 4 ? 5 : 4))) vote_kernel(const VoteArgs a) {
     constexpr int SW = VoteGeom<R>::SW, SH = VoteGeom<R>::SH, OFF = VoteGeom<R>::OFF, SWP = VoteGeom<R>::SWP;
     __shared__ __align__(16) uint32_t sc[SH][SWP];
     __shared__ VoteShared<R> S;
