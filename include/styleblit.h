@@ -77,8 +77,8 @@ typedef enum {
 #define SB_MAX_DIM 65535      /* image sides W, H in [1, SB_MAX_DIM] (target and source)      */
 #define SB_MAX_LEVELS 15      /* level l uses spacing h = 2^l, l in [1, SB_MAX_LEVELS]; L <= 9
                                  on the tiled kernel, L in 10..15 on the per-pixel kernel     */
-#define SB_MAX_RADIUS 8       /* voting radius r in [0, SB_MAX_RADIUS]; r <= 7 on the 16-bit
-                                 SWAR vote kernels, r = 8 on the 32-bit per-pixel vote       */
+#define SB_MAX_RADIUS 8       /* voting radius r in [0, SB_MAX_RADIUS]; the tiled SWAR vote sums
+                                 16-bit lanes (r = 8: two lane pairs, dy < 0 and dy >= 0)     */
 
 typedef struct {
     /* t: the threshold of Alg. 2 line 385 ("e < t"), in 8-bit guide units.  The error e is

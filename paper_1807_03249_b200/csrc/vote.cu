@@ -23,8 +23,8 @@
 //      vote for the same source pixel, and each run costs one gather weighted by its length.
 //      Pixels whose rows have at most two runs (most) take a branch-free two-gather row
 //      step; the others a run loop, in their own queue so warps do not diverge.  Sums are
-//      SWAR (two 16-bit lanes per register; (2r+1)^2 * 255 < 2^16 for r <= 7); division by
-//      (2r+1)^2.
+//      SWAR (two 16-bit lanes per register; (2r+1)^2 * 255 < 2^16 for r <= 7, r = 8 splits the
+//      window rows over two register pairs); division by (2r+1)^2.
 // Border tiles: every pixel takes the general per-position path with target clipping and
 // source bounds tests on packed coordinates (x | y<<16; for W, H <= 32767 and |d| <= 2r the
 // packed sum src(q) + (p-q) never carries between fields and any position left of / above
@@ -50,25 +50,52 @@ constexpr int NG = TW / 4;                   // 4-pixel groups per row
 // offset, so the packed in-source test rejects it by itself (and it never links with a coordinate)
 constexpr uint32_t kOutside = 0xC000C000u;
 
-__device__ __forceinline__ uint32_t finish(uint32_t lo, uint32_t hi, uint32_t n) {
-    if (n <= 1) return (lo & 0x00FF00FFu) | ((hi & 0x00FF00FFu) << 8);
+// The colour sums of one pixel's window: two 16-bit lanes per register (SWAR, channels 0 and 2
+// in lo, 1 and 3 in hi).  For r = 8 a lane could overflow ((2r+1)^2 * 255 >= 2^16): the window
+// rows dy < 0 and dy >= 0 then sum into separate pairs (at most 9 * 17 * 255 < 2^16 each) that
+// meet in 32 bits at the end.  dy is a compile-time constant at every call (unrolled loops).
+template <int R>
+struct Sums {
+    static constexpr bool SPLIT = (2 * R + 1) * (2 * R + 1) * 255 >= 65536;
+    uint32_t lo = 0, hi = 0, lo2 = 0, hi2 = 0;
+    __device__ __forceinline__ void add(int dy, uint32_t c, uint32_t len) {
+        const uint32_t l = (c & 0x00FF00FFu) * len, h = __byte_perm(c, 0u, 0x7371) * len;  // bytes 1, 3
+        if (SPLIT && dy >= 0) {
+            lo2 += l;
+            hi2 += h;
+        } else {
+            lo += l;
+            hi += h;
+        }
+    }
+    __device__ __forceinline__ void channels(uint32_t (&s)[4]) const {
+        s[0] = lo & 0xFFFFu; s[1] = hi & 0xFFFFu; s[2] = lo >> 16; s[3] = hi >> 16;
+        if (SPLIT) { s[0] += lo2 & 0xFFFFu; s[1] += hi2 & 0xFFFFu; s[2] += lo2 >> 16; s[3] += hi2 >> 16; }
+    }
+};
+
+template <int R>
+__device__ __forceinline__ uint32_t finish(const Sums<R>& sm, uint32_t n) {
+    uint32_t s[4];
+    sm.channels(s);
+    if (n <= 1) return s[0] | (s[1] << 8) | (s[2] << 16) | (s[3] << 24);
     const uint32_t half = n >> 1;
-    const uint32_t m = 0xFFFFFFFFu / n + 1u;  // ceil(2^32/n): exact floor for numerators < 2^17
-    const uint32_t c0 = __umulhi((lo & 0xFFFFu) + half, m);
-    const uint32_t c1 = __umulhi((hi & 0xFFFFu) + half, m);
-    const uint32_t c2 = __umulhi((lo >> 16) + half, m);
-    const uint32_t c3 = __umulhi((hi >> 16) + half, m);
-    return c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
+    const uint32_t m = 0xFFFFFFFFu / n + 1u;  // ceil(2^32/n): exact floor for numerators < 2^32/n
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c |= __umulhi(s[k] + half, m) << (8 * k);
+    return c;
 }
 
-template <uint32_t N>
-__device__ __forceinline__ uint32_t finish_const(uint32_t lo, uint32_t hi) {
+template <uint32_t N, int R>
+__device__ __forceinline__ uint32_t finish_const(const Sums<R>& sm) {
     constexpr uint32_t half = N / 2;
-    const uint32_t c0 = ((lo & 0xFFFFu) + half) / N;
-    const uint32_t c1 = ((hi & 0xFFFFu) + half) / N;
-    const uint32_t c2 = ((lo >> 16) + half) / N;
-    const uint32_t c3 = ((hi >> 16) + half) / N;
-    return c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
+    uint32_t s[4];
+    sm.channels(s);
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c |= ((s[k] + half) / N) << (8 * k);
+    return c;
 }
 
 // Predicated gather: returns 0 without touching memory when !pred (keeps L1 traffic to the
@@ -82,10 +109,6 @@ __device__ __forceinline__ uint32_t ldg_if(const uint32_t* p, bool pred) {
     return v;
 }
 
-__device__ __forceinline__ void swar_add(uint32_t c, uint32_t& lo, uint32_t& hi) {
-    lo += c & 0x00FF00FFu;
-    hi += __byte_perm(c, 0u, 0x7371);  // bytes 1 and 3 into 16-bit lanes
-}
 }  // namespace
 
 // Tile geometry and the shared scratch of one tile (besides the staged coordinates).
@@ -285,7 +308,7 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
             const int idx = queue[j];
             SB_CHECK(idx >= 0 && idx < TH * TW, "two-run queue");
             const int ry = idx / TW, x = idx - ry * TW;
-            uint32_t lo = 0, hi = 0;
+            Sums<R> sum;
 #pragma unroll
             for (int dy = -R; dy <= R; ++dy) {
                 const int yy = ry + R + dy;
@@ -302,10 +325,10 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
                 const uint32_t col1 = __ldg(cs + (row[0] - shy + (uint32_t)R));
                 const uint32_t c2 = W - c1;
                 const uint32_t col2 = ldg_if(cs + (row[h2] - shy - (h2 - (uint32_t)R)), c2 != 0);
-                lo += (col1 & 0x00FF00FFu) * c1 + (col2 & 0x00FF00FFu) * c2;
-                hi += __byte_perm(col1, 0u, 0x7371) * c1 + __byte_perm(col2, 0u, 0x7371) * c2;
+                sum.add(dy, col1, c1);
+                sum.add(dy, col2, c2);
             }
-            outc[ry][x] = finish_const<W * W>(lo, hi);
+            outc[ry][x] = finish_const<W * W>(sum);
         }
         // ---- 3b. pixels with a row of three or more runs: the general run loop
         const int n3 = qn3;
@@ -313,7 +336,7 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
             const int idx = queue[TH * TW - 1 - j];
             SB_CHECK(idx >= 0 && idx < TH * TW, "run-loop queue");
             const int ry = idx / TW, x = idx - ry * TW;
-            uint32_t lo = 0, hi = 0;
+            Sums<R> sum;
 #pragma unroll
             for (int dy = -R; dy <= R; ++dy) {
                 const int yy = ry + R + dy;
@@ -327,20 +350,16 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
                     const uint32_t k = __ffs(m) - 1;
                     SB_CHECK(src_in(pos), "run gather");
                     const uint32_t c = __ldg(cs + pos);
-                    const uint32_t len = k + 1 - start;
-                    lo += (c & 0x00FF00FFu) * len;
-                    hi += __byte_perm(c, 0u, 0x7371) * len;
+                    sum.add(dy, c, k + 1 - start);
                     start = k + 1;
                     m &= m - 1;
                     pos = row[start] - shy - (start - (uint32_t)R);
                 }
                 SB_CHECK(src_in(pos), "last-run gather");
                 const uint32_t c = __ldg(cs + pos);
-                const uint32_t len = W - start;
-                lo += (c & 0x00FF00FFu) * len;
-                hi += __byte_perm(c, 0u, 0x7371) * len;
+                sum.add(dy, c, W - start);
             }
-            outc[ry][x] = finish_const<W * W>(lo, hi);
+            outc[ry][x] = finish_const<W * W>(sum);
         }
         // ---- 3c. frame-edge pixels of a fast tile: the general per-position path (clipped window)
         if (edge_tile) {
@@ -350,7 +369,8 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
                 const int idx = qe[j];
                 SB_CHECK(idx >= 0 && idx < TH * TW, "edge queue");
                 const int ry = idx / TW, x = idx - ry * TW;
-                uint32_t lo = 0, hi = 0, cnt = 0;
+                Sums<R> sum;
+                uint32_t cnt = 0;
 #pragma unroll
                 for (int dy = -R; dy <= R; ++dy) {
 #pragma unroll
@@ -367,10 +387,10 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
                         }
                         SB_CHECK(!in || src_in(li), "edge gather");
                         const uint32_t c = ldg_if(cs + (in ? li : 0u), in);
-                        if (in) { swar_add(c, lo, hi); ++cnt; }
+                        if (in) { sum.add(dy, c, 1u); ++cnt; }
                     }
                 }
-                outc[ry][x] = finish(lo, hi, cnt);
+                outc[ry][x] = finish(sum, cnt);
             }
         }
     } else {
@@ -381,7 +401,8 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
             const int ry = idx / TW, x = idx - ry * TW;
             const int gx = x0 + x;
             if (y0 + ry >= a.row_end || gx >= a.wt) continue;
-            uint32_t lo = 0, hi = 0, cnt = 0;
+            Sums<R> sum;
+            uint32_t cnt = 0;
 #pragma unroll
             for (int dy = -R; dy <= R; ++dy) {
                 const uint32_t sh = (uint32_t)dy << 16;
@@ -394,10 +415,10 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
                     asm("min.u16x2 %0, %1, %2;" : "=r"(mn) : "r"(pos), "r"(lim));
                     const bool in = mn == pos;
                     const uint32_t c = __ldg(cs + (in ? (PAD ? pos : (pos >> 16) * ws + (pos & 0xFFFFu)) : 0u));
-                    if (in) { swar_add(c, lo, hi); ++cnt; }
+                    if (in) { sum.add(dy, c, 1u); ++cnt; }
                 }
             }
-            outc[ry][x] = finish(lo, hi, cnt);  // cnt >= 1: q = p votes for src(p)
+            outc[ry][x] = finish(sum, cnt);  // cnt >= 1: q = p votes for src(p)
         }
     }
     __syncthreads();
@@ -694,9 +715,9 @@ static bool launch_tma_r(const VoteArgs& a, int n_frames, cudaStream_t st) {
 }
 
 cudaError_t launch_vote(const VoteArgs& a, int n_frames, cudaStream_t st, int* launches) {
-    // r = 8 or a side beyond 32767: the per-pixel vote of vote_wide.cu (32-bit sums, signed
-    // coordinates); everything else runs on the packed-arithmetic kernels below
-    if (a.r > 7 || a.wt > kPackedMaxDim || a.ht > kPackedMaxDim || a.ws > kPackedMaxDim || a.hs > kPackedMaxDim)
+    // a side beyond 32767: the per-pixel vote of vote_wide.cu (32-bit sums, signed coordinates);
+    // everything else runs on the packed-arithmetic kernels below
+    if (a.r > 8 || a.wt > kPackedMaxDim || a.ht > kPackedMaxDim || a.ws > kPackedMaxDim || a.hs > kPackedMaxDim)
         return launch_vote_wide(a, n_frames, st, launches);
     // A/B alternatives for r = 1, 2 (measured slower): SB_VOTE=peel the peel vote
     // of vote_peel.cu, SB_VOTE=hist the offset-histogram vote of vote_hist.cu.
@@ -722,7 +743,7 @@ cudaError_t launch_vote(const VoteArgs& a, int n_frames, cudaStream_t st, int* l
             case 2: done = launch_tma_r<2>(a, n_frames, st); break;
             case 3: done = launch_tma_r<3>(a, n_frames, st); break;
             case 4: done = launch_tma_r<4>(a, n_frames, st); break;
-            case 5: case 6: case 7: break;  // two staging buffers exceed 48 KB of static shared memory
+            case 5: case 6: case 7: case 8: break;  // two staging buffers exceed 48 KB of static shared memory
             default: return cudaErrorInvalidValue;
         }
         if (done) {
@@ -741,6 +762,7 @@ cudaError_t launch_vote(const VoteArgs& a, int n_frames, cudaStream_t st, int* l
         case 5: launch_r<5>(a, grid, st); break;
         case 6: launch_r<6>(a, grid, st); break;
         case 7: launch_r<7>(a, grid, st); break;
+        case 8: launch_r<8>(a, grid, st); break;
         default: return cudaErrorInvalidValue;
     }
     *launches += 1;

@@ -1,6 +1,6 @@
 // vote_wide.cu -- the voting step of PAPER.md:412-421 for the regimes the packed-arithmetic vote
-// kernels (vote.cu) do not serve: r = 8 ((2r+1)^2 * 255 exceeds the 16-bit SWAR lanes) and
-// images wider or taller than 32767 pixels (packed coordinates would carry between fields).
+// kernels (vote.cu) do not serve: images wider or taller than 32767 pixels (packed coordinates
+// would carry between fields).  (Up to round 2 it also served r = 8.)
 //
 // One thread per output pixel of a 32 x 8 tile; the tile's coordinates plus an r halo are
 // staged in shared memory (kOutside outside the target: a valid coordinate has x <= 65534);

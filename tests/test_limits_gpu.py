@@ -1,7 +1,8 @@
-"""GPU parity at the edges of the SURVEY 8(b) contract that the tiled, packed-coordinate kernels
-do not serve and the per-pixel kernels do (include/styleblit.h: SB_MAX_DIM, SB_MAX_LEVELS,
-SB_MAX_RADIUS): image sides beyond 32767, L = 10..15 and the vote radius r = 8.  Every case is
-compared with the CPU oracle element by element (coords, levels, colours bit-exact)."""
+"""GPU parity at the edges of the SURVEY 8(b) contract (include/styleblit.h: SB_MAX_DIM,
+SB_MAX_LEVELS, SB_MAX_RADIUS): image sides beyond 32767 and L = 10..15 (the per-pixel kernels),
+and the vote radius r = 8 (the runs kernel with its window sums split over two SWAR register
+pairs).  Every case is compared with the CPU oracle element by element (coords, levels, colours
+bit-exact)."""
 import os
 
 import numpy as np
@@ -53,11 +54,29 @@ def test_deep_hierarchies(L):
 
 @pytest.mark.parametrize("r", [7, 8])
 def test_radius_8(r):
-    """r = 8 ((2r+1)^2 * 255 > 2^16: the 32-bit per-pixel vote) next to r = 7 (SWAR kernel)."""
+    """r = 8 ((2r+1)^2 * 255 > 2^16: the runs kernel splits the window rows over two SWAR register
+    pairs) next to r = 7 (one pair); a target with interior fast tiles and frame-edge tiles."""
     cs, gs = _exemplar()
-    gt = synth.heightfield_normals(150, 70, seed=1).numpy()
-    _both(cs, gs, gt, t=32.0, L=3, r=r)
-    _both(cs, gs, gt, t=32.0, L=3, r=r, with_exemplar=True)
+    for wt, ht in ((150, 70), (300, 100)):
+        gt = synth.heightfield_normals(wt, ht, seed=1).numpy()
+        _both(cs, gs, gt, t=32.0, L=3, r=r)
+        _both(cs, gs, gt, t=32.0, L=3, r=r, with_exemplar=True)
+
+
+@pytest.mark.parametrize("with_exemplar", [False, True])
+def test_radius_8_saturated_sums(with_exemplar):
+    """r = 8 where every channel sum reaches 289 * 255 = 73695 > 2^16 (a white exemplar with a few
+    dark pixels; noise guides: many short chunks, so the two-run, run-loop and border paths all
+    carry saturated sums)."""
+    rng = np.random.RandomState(8)
+    cs = np.full((96, 96, 4), 255, np.uint8)
+    cs[rng.rand(96, 96) < 0.02] = 0
+    gs = rng.randint(0, 256, (96, 96, 4)).astype(np.uint8)
+    gt = rng.randint(0, 256, (80, 260, 4)).astype(np.uint8)
+    _both(cs, gs, gt, t=2000.0, L=2, r=8, with_exemplar=with_exemplar)
+    gs_smooth = synth.heightfield_normals(96, 96, seed=3).numpy()
+    gt_smooth = synth.heightfield_normals(260, 80, seed=4).numpy()
+    _both(cs, gs_smooth, gt_smooth, t=20.0, L=3, r=8, with_exemplar=with_exemplar)
 
 
 @pytest.mark.parametrize("wt,ht", [(40000, 3), (5, 33000)])
