@@ -68,6 +68,18 @@ struct Sums {
             hi += h;
         }
     }
+    // two colours with their counts (the two runs of a window row), summed before the accumulator
+    __device__ __forceinline__ void add2(int dy, uint32_t c1, uint32_t n1, uint32_t c2, uint32_t n2) {
+        const uint32_t l = (c1 & 0x00FF00FFu) * n1 + (c2 & 0x00FF00FFu) * n2;
+        const uint32_t h = __byte_perm(c1, 0u, 0x7371) * n1 + __byte_perm(c2, 0u, 0x7371) * n2;
+        if (SPLIT && dy >= 0) {
+            lo2 += l;
+            hi2 += h;
+        } else {
+            lo += l;
+            hi += h;
+        }
+    }
     __device__ __forceinline__ void channels(uint32_t (&s)[4]) const {
         s[0] = lo & 0xFFFFu; s[1] = hi & 0xFFFFu; s[2] = lo >> 16; s[3] = hi >> 16;
         if (SPLIT) { s[0] += lo2 & 0xFFFFu; s[1] += hi2 & 0xFFFFu; s[2] += lo2 >> 16; s[3] += hi2 >> 16; }
@@ -78,13 +90,13 @@ template <int R>
 __device__ __forceinline__ uint32_t finish(const Sums<R>& sm, uint32_t n) {
     uint32_t s[4];
     sm.channels(s);
-    if (n <= 1) return s[0] | (s[1] << 8) | (s[2] << 16) | (s[3] << 24);
+    if (n <= 1) return Sums<R>::SPLIT ? s[0] | (s[1] << 8) | (s[2] << 16) | (s[3] << 24)
+                                      : (sm.lo & 0x00FF00FFu) | ((sm.hi & 0x00FF00FFu) << 8);
     const uint32_t half = n >> 1;
     const uint32_t m = 0xFFFFFFFFu / n + 1u;  // ceil(2^32/n): exact floor for numerators < 2^32/n
-    uint32_t c = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) c |= __umulhi(s[k] + half, m) << (8 * k);
-    return c;
+    const uint32_t c0 = __umulhi(s[0] + half, m), c1 = __umulhi(s[1] + half, m);
+    const uint32_t c2 = __umulhi(s[2] + half, m), c3 = __umulhi(s[3] + half, m);
+    return c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
 }
 
 template <uint32_t N, int R>
@@ -92,10 +104,9 @@ __device__ __forceinline__ uint32_t finish_const(const Sums<R>& sm) {
     constexpr uint32_t half = N / 2;
     uint32_t s[4];
     sm.channels(s);
-    uint32_t c = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) c |= ((s[k] + half) / N) << (8 * k);
-    return c;
+    const uint32_t c0 = (s[0] + half) / N, c1 = (s[1] + half) / N;
+    const uint32_t c2 = (s[2] + half) / N, c3 = (s[3] + half) / N;
+    return c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
 }
 
 // Predicated gather: returns 0 without touching memory when !pred (keeps L1 traffic to the
@@ -325,8 +336,7 @@ __device__ __forceinline__ void vote_tile(const VoteArgs& a, uint32_t (*sc)[Vote
                 const uint32_t col1 = __ldg(cs + (row[0] - shy + (uint32_t)R));
                 const uint32_t c2 = W - c1;
                 const uint32_t col2 = ldg_if(cs + (row[h2] - shy - (h2 - (uint32_t)R)), c2 != 0);
-                sum.add(dy, col1, c1);
-                sum.add(dy, col2, c2);
+                sum.add2(dy, col1, c1, col2, c2);
             }
             outc[ry][x] = finish_const<W * W>(sum);
         }
