@@ -85,11 +85,14 @@ sb_status validate(const sb_params* prm, int32_t n_frames, const uint8_t* cs, co
     if (!cs) return fail(SB_EINVAL, "cs (style exemplar C_S) is NULL");
     if (!gs) return fail(SB_EINVAL, "gs (source guide G_S) is NULL");
     if (!lut) return fail(SB_EINVAL, "lut is NULL");
-    if (!gt) return fail(SB_EINVAL, "gt (target guide G_T) is NULL");
+    // per-frame buffers of an empty batch hold zero bytes: NULL is then valid for them
+    const bool frames = n_frames > 0;
+    if (!gt && frames) return fail(SB_EINVAL, "gt (target guide G_T) is NULL");
     const bool no_color = (prm->flags & SB_NO_COLOR) != 0;
     const int r = prm->blend_radius;
-    if (!no_color && !ct) return fail(SB_EINVAL, "ct is NULL (pass SB_NO_COLOR to skip colours)");
-    if (r > 0 && !no_color && !coords) return fail(SB_EINVAL, "coords is NULL but blend_radius=%d needs it", r);
+    if (!no_color && !ct && frames) return fail(SB_EINVAL, "ct is NULL (pass SB_NO_COLOR to skip colours)");
+    if (r > 0 && !no_color && !coords && frames)
+        return fail(SB_EINVAL, "coords is NULL but blend_radius=%d needs it", r);
     if (device_outputs) {
         if (!aligned16(cs) || !aligned16(gs) || !aligned16(gt) || (ct && !aligned16(ct)) ||
             (coords && !aligned16(coords)) || !aligned16(lut) || (prm->exemplar && !aligned16(prm->exemplar)))
@@ -293,10 +296,10 @@ sb_status sb_vote(const uint32_t* coords, int32_t n_frames, int32_t wt, int32_t 
                   void* stream) {
     g_launches = 0;
     sb_status s;
-    if (!coords) return fail(SB_EINVAL, "coords is NULL");
-    if (!cs) return fail(SB_EINVAL, "cs (style exemplar C_S) is NULL");
-    if (!ct) return fail(SB_EINVAL, "ct is NULL");
     if (n_frames < 0) return fail(SB_EINVAL, "n_frames=%d < 0", n_frames);
+    if (!coords && n_frames > 0) return fail(SB_EINVAL, "coords is NULL");  // NULL is valid for 0 frames
+    if (!cs) return fail(SB_EINVAL, "cs (style exemplar C_S) is NULL");
+    if (!ct && n_frames > 0) return fail(SB_EINVAL, "ct is NULL");
     if ((s = check_dims("source (ws,hs)", ws, hs)) != SB_OK) return s;
     if ((s = check_dims("target (wt,ht)", wt, ht)) != SB_OK) return s;
     if (r < 0 || r > SB_MAX_RADIUS) return fail(SB_EINVAL, "r=%d outside [0,%d]", r, SB_MAX_RADIUS);
@@ -338,8 +341,8 @@ sb_status sb_stylize_batch_host(const sb_params* prm, int32_t n_frames, const ui
     if (n_frames < 0) return fail(SB_EINVAL, "n_frames=%d < 0", n_frames);
     if (depth < 1 || depth > 8) return fail(SB_EINVAL, "depth=%d outside [1,8]", depth);
     if (!workspace) return fail(SB_EINVAL, "workspace is NULL");
-    if (!gt_host) return fail(SB_EINVAL, "gt_host is NULL");
-    if (!ct_host && !(prm && (prm->flags & SB_NO_COLOR))) return fail(SB_EINVAL, "ct_host is NULL");
+    if (!gt_host && n_frames > 0) return fail(SB_EINVAL, "gt_host is NULL");  // NULL is valid for 0 frames
+    if (!ct_host && n_frames > 0 && !(prm && (prm->flags & SB_NO_COLOR))) return fail(SB_EINVAL, "ct_host is NULL");
     if (workspace_bytes < sb_host_workspace_bytes(wt, ht, prm ? prm->blend_radius : 0, depth))
         return fail(SB_EINVAL, "workspace_bytes=%zu < sb_host_workspace_bytes()=%zu", workspace_bytes,
                     sb_host_workspace_bytes(wt, ht, prm ? prm->blend_radius : 0, depth));

@@ -119,10 +119,24 @@ def test_vote_needs_coords(lib):
 
 
 def test_no_color_allows_null_ct(lib):
-    # ct may be NULL with SB_NO_COLOR; n_frames = 0 means nothing is launched
+    # ct may be NULL with SB_NO_COLOR: validation passes (on this GPU-less host the launch then
+    # fails with SB_ECUDA); without the flag the same call is SB_EINVAL naming ct
     p = _prm(flags=_lib.SB_NO_COLOR)
-    st = lib.sb_stylize_batch(C.byref(p), 0, None, FAKE, FAKE, 64, 64, FAKE, FAKE, 64, 64, 0, FAKE, 0, None)
-    assert st == _lib.SB_OK
+    st = lib.sb_stylize(C.byref(p), FAKE, FAKE, 64, 64, FAKE, FAKE, 64, 64, 0, FAKE, 0, None)
+    assert st != _lib.SB_EINVAL, lib.sb_last_error().decode()
+    st = lib.sb_stylize(C.byref(_prm()), FAKE, FAKE, 64, 64, FAKE, FAKE, 64, 64, 0, FAKE, 0, None)
+    assert st == _lib.SB_EINVAL and "ct" in lib.sb_last_error().decode()
+
+
+def test_empty_batch_allows_null_frame_buffers(lib):
+    """n_frames = 0: the per-frame buffers hold zero bytes and may be NULL (styleblit.h); the
+    exemplar-level inputs are still required; nothing is launched."""
+    p = _prm(blend_radius=2)
+    assert lib.sb_stylize_batch(C.byref(p), 0, None, FAKE, FAKE, 64, 64, FAKE, 0, 64, 64, 0, 0, 0, None) == _lib.SB_OK
+    assert lib.sb_last_launch_count() == 0
+    assert lib.sb_stylize_batch(C.byref(p), 0, None, 0, FAKE, 64, 64, FAKE, 0, 64, 64, 0, 0, 0, None) == _lib.SB_EINVAL
+    assert lib.sb_vote(0, 0, 64, 64, FAKE, 64, 64, 2, 0, 0, 0, None, None) == _lib.SB_OK
+    assert lib.sb_vote(0, 1, 64, 64, FAKE, 64, 64, 2, 0, 0, 0, None, None) == _lib.SB_EINVAL
 
 
 def test_build_lut_invalid(lib):

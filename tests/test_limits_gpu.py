@@ -120,3 +120,24 @@ def test_host_pipeline_at_the_limits(L, r, wt, ht):
                        gt[1], nthreads=NTH)
     want = oracle.vote(o[1], cs, r, nthreads=NTH) if r > 0 else o[0]
     assert (ct_h[1].numpy() == want).all()
+
+
+def test_empty_batches():
+    """n_frames = 0 (an empty batch is valid): the device batch, the vote and the
+    host pipeline return SB_OK, launch no kernel and leave their outputs untouched."""
+    cs, gs = _exemplar()
+    csd, gsd = torch.from_numpy(cs).cuda(), torch.from_numpy(gs).cuda()
+    lut = sb.build_lut(gsd)
+    gt = torch.zeros(0, 48, 64, 4, dtype=torch.uint8, device="cuda")
+    ct = torch.zeros(0, 48, 64, 4, dtype=torch.uint8, device="cuda")
+    co = torch.zeros(0, 48, 64, dtype=torch.int32, device="cuda")
+    prm = sb.Params(threshold=20.0, levels=4, blend_radius=2, guide_channels=3, seed=3)
+    sb.stylize_batch(prm, csd, gsd, lut, gt, ct=ct, coords=co, want_level=False)
+    assert sb.launch_count() == 0
+    sb.vote(co, csd, 2, ct=ct)
+    assert sb.launch_count() == 0
+    gt_h = torch.zeros(0, 48, 64, 4, dtype=torch.uint8).pin_memory()
+    ct_h = torch.zeros(0, 48, 64, 4, dtype=torch.uint8).pin_memory()
+    sb.stylize_batch_host(sb.Params(threshold=20.0, levels=4, guide_channels=3, seed=3), csd, gsd, lut, gt_h, ct_h)
+    assert sb.launch_count() == 0
+    torch.cuda.synchronize()
