@@ -141,3 +141,18 @@ def test_empty_batches():
     sb.stylize_batch_host(sb.Params(threshold=20.0, levels=4, guide_channels=3, seed=3), csd, gsd, lut, gt_h, ct_h)
     assert sb.launch_count() == 0
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("ws,hs,wt,ht", [(1, 1, 1, 1), (1, 1, 37, 5), (5, 1, 1, 9), (1, 7, 131, 1), (2, 2, 3, 130),
+                                         (17, 17, 1, 1)])
+@pytest.mark.parametrize("L,r", [(1, 0), (5, 2), (15, 8)])
+def test_degenerate_sizes(ws, hs, wt, ht, L, r):
+    """Single-pixel and single-row/column exemplars and targets (every window clipped, no source
+    margin for the fast vote tiles, seed cells far larger than the image) at the ends of the L
+    and r ranges: bit-exact against the oracle, with and without the strided exemplar copy."""
+    rng = np.random.RandomState(ws * 1000 + hs * 100 + wt + ht)
+    cs = rng.randint(0, 256, (hs, ws, 4)).astype(np.uint8)
+    gs = rng.randint(0, 256, (hs, ws, 4)).astype(np.uint8)
+    gt = rng.randint(0, 256, (ht, wt, 4)).astype(np.uint8)
+    for ex in (False, True):
+        _both(cs, gs, gt, t=90.0, L=L, r=r, with_exemplar=ex)
