@@ -51,7 +51,7 @@ case = st.fixed_dictionaries({
 })
 
 
-@settings(max_examples=150, derandomize=True, deadline=None,
+@settings(max_examples=int(os.environ.get("SB_HYP_N", "150")), derandomize=os.environ.get("SB_HYP_RANDOM") is None, deadline=None,
           suppress_health_check=[HealthCheck.too_slow, HealthCheck.data_too_large])
 @given(c=case)
 def test_random_parity(c):
@@ -68,7 +68,7 @@ def test_random_parity(c):
         gs[..., 3] = (np.arange(ws)[None, :] * 4 // max(ws, 1) * 50).astype(np.uint8)
         gt[..., 3] = (np.arange(wt)[None, :] * 4 // max(wt, 1) * 50).astype(np.uint8)
     w = c["weights"]
-    rb = int(c["rows"][0] * ht) if c["strip"] else 0
+    rb = min(int(c["rows"][0] * ht), ht - 1) if c["strip"] else 0  # a non-empty strip
     re_ = max(rb + 1, int(round(c["rows"][1] * ht))) if c["strip"] else ht
     re_ = min(re_, ht)
     r = c["r"]
