@@ -7,7 +7,9 @@ synthetic guides), L in 1..15, t (including 0 and values between integers), C in
 radius r in 0..8, the jitter seed, zero jitter, per-channel weights, a segmentation label byte,
 the exact three-channel search (SB_LUT_RGB), an output strip [row_begin, row_end) and the
 strided exemplar copy.  The CUDA path and the oracle must agree bit for bit on the coordinates,
-the levels and the colours (blit or vote) of every row the call writes.
+the levels and the colours (blit or vote) of every row the call writes.  test_random_parity_large
+redraws the sizes at multi-tile scale (targets up to 1280 x 200, exemplars up to 512^2, L 3..9).
+SB_HYP_N / SB_HYP_N_LARGE set the example counts, SB_HYP_RANDOM=1 draws fresh examples.
 """
 import os
 
@@ -55,6 +57,28 @@ case = st.fixed_dictionaries({
           suppress_health_check=[HealthCheck.too_slow, HealthCheck.data_too_large])
 @given(c=case)
 def test_random_parity(c):
+    _check(c)
+
+
+# multi-tile frames (up to 10 x 13 tiles) and exemplars up to 512^2: the interior fast paths of
+# both kernels, the level tables at L up to 9 and long group / pixel queues
+large_sizes = st.fixed_dictionaries({
+    "wt": st.integers(129, 1280), "ht": st.integers(17, 200), "ws": st.integers(64, 512), "hs": st.integers(64, 512),
+    "L": st.integers(3, 9),
+})
+
+
+@settings(max_examples=int(os.environ.get("SB_HYP_N_LARGE", "12")), derandomize=os.environ.get("SB_HYP_RANDOM") is None,
+          deadline=None, suppress_health_check=[HealthCheck.too_slow, HealthCheck.data_too_large])
+@given(c=case, big=large_sizes)
+def test_random_parity_large(c, big):
+    c = dict(c)
+    c.update(big)
+    c["lut_rgb"] = False  # the oracle's exact three-channel search is quadratic in the exemplar
+    _check(c)
+
+
+def _check(c):
     rng = np.random.RandomState(c["rng"])
     wt, ht, ws, hs = c["wt"], c["ht"], c["ws"], c["hs"]
     if c["lut_rgb"]:  # the oracle searches all exemplar pixels per query: keep it small
