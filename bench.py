@@ -64,6 +64,7 @@ def parse():
                          "ragged width) and their oracle timings")
     ap.add_argument("--config-steps", type=int, default=10, help="timed steps of each per-config section")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-digest", action="store_true", help="skip the output_sha1 digests of global frames 0, B-1")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
@@ -515,6 +516,14 @@ def run_ours(args):
 
     r = args.blend_radius
     main = time_path(r, args.steps, args.warmup)
+    # determinism across GPU counts: SHA-1 of the C_T of global frames 0 and B-1,
+    # which rank 0 holds at every N (frame mode: its own first frames; strip mode: the gathered
+    # frames) with the same inputs and seeds -- the digests must not change with N
+    digests = None
+    if rank == 0 and not args.no_digest:
+        import hashlib
+        torch.cuda.synchronize(dev)
+        digests = {f"frame_{i}": hashlib.sha1(ct[i].cpu().numpy().tobytes()).hexdigest()[:16] for i in (0, B - 1)}
     ms_step, value, dom, kt, alg = main["ms_step"], main["value"], main["dom"], main["kt"], main["alg"]
     hbm, hbm_src = peaks()
     ach = alg[dom] / (kt[dom] * 1e-3) / 1e9
@@ -691,6 +700,7 @@ def run_ours(args):
                      "alg_bytes_per_launch": alg[dom], "alg_bytes_per_px": alg[dom] // px_step},
         "gpu_launches": main["launches"],
         "clocks": main["clocks"],
+        "output_sha1": digests,
         "e2e": e2e,
         "e2e_rgb": e2e_rgb,
         "blend_r2": blend,
