@@ -30,6 +30,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -173,7 +175,8 @@ def gpu_section(torch, sb, synth, dev, stream, hbm, cid, frames, rad, steps, war
     gt = torch.empty(frames, ht, wt, 4, dtype=torch.uint8, device=dev)
     for i in range(frames):
         gt[i] = firsts[i % len(firsts)]
-    seeds = [(cfg["seed"] + i) & 0xFFFFFFFF for i in range(frames)]
+    # a host uint32 array built once: the binding passes it to the ABI without per-step conversion
+    seeds = ((cfg["seed"] + np.arange(frames, dtype=np.int64)) & 0xFFFFFFFF).astype(np.uint32)
     lut = torch.empty(65536, dtype=torch.int32, device=dev)
     lut_ws = torch.empty(sb.lib().sb_lut_workspace_bytes(), dtype=torch.uint8, device=dev)
     ex = torch.empty(sb.exemplar_bytes(cfg["ws"], cfg["hs"]), dtype=torch.uint8, device=dev)
@@ -412,7 +415,7 @@ def run_ours(args):
             gt[i] = gt[i % n_distinct]
     rb, re_ = sharding.strip_rows(HT, world, rank) if strip else (0, HT)
     frame0 = 0 if strip else rank * B
-    seeds = [(cfg["seed"] + frame0 + i) & 0xFFFFFFFF for i in range(B)]
+    seeds = ((cfg["seed"] + frame0 + np.arange(B, dtype=np.int64)) & 0xFFFFFFFF).astype(np.uint32)
     coords = torch.empty(B, HT, WT, dtype=torch.int32, device=dev)
     ct = torch.empty(B, HT, WT, 4, dtype=torch.uint8, device=dev)
     lut = torch.empty(65536, dtype=torch.int32, device=dev)

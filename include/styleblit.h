@@ -184,7 +184,9 @@ sb_status sb_stylize(const sb_params* prm,
 
 /* n_frames frames of wt x ht (contiguous), frame i jittered with frame_seeds[i]
  * (HOST array of n_frames; NULL => prm->seed + i mod 2^32).  Same buffers and rules as
- * sb_stylize, each with n_frames frames.  n_frames = 0 is a valid empty batch: SB_OK, no
+ * sb_stylize, each with n_frames frames.  Seeds of the form s0 + i (mod 2^32) -- NULL, or an
+ * explicit array of that form -- run as one launch per 65535 frames; other seed arrays as one
+ * launch per 512 frames (they travel in the kernel parameters).  n_frames = 0 is a valid empty batch: SB_OK, no
  * launch, and the per-frame buffers (gt, ct, coords, level) may then be NULL (likewise for
  * sb_vote and sb_stylize_batch_host).                                                     */
 sb_status sb_stylize_batch(const sb_params* prm, int32_t n_frames, const uint32_t* frame_seeds,

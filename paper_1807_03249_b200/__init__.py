@@ -15,6 +15,7 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -182,12 +183,26 @@ def _check_exemplar(ex: torch.Tensor | None, ws: int, hs: int, device) -> None:
 
 
 def _seeds(frame_seeds, n: int):
+    """frame_seeds -> a HOST uint32 array the ABI reads during the call.  A contiguous 1-D numpy
+    uint32 array (or CPU uint32-compatible tensor) is passed without copying; other sequences
+    are reduced mod 2^32 (a 4096-entry Python list costs ~0.1 ms; precompute arrays in loops)."""
     if frame_seeds is None:
         return None
-    seeds = [int(s) & 0xFFFFFFFF for s in frame_seeds]
-    if len(seeds) != n:
-        raise ValueError(f"frame_seeds has {len(seeds)} entries for {n} frames")
-    return (C.c_uint32 * n)(*seeds)
+    if isinstance(frame_seeds, torch.Tensor):
+        if frame_seeds.is_cuda:
+            raise ValueError("frame_seeds must be a HOST array")
+        frame_seeds = frame_seeds.numpy()
+    if isinstance(frame_seeds, np.ndarray) and frame_seeds.dtype == np.uint32 and frame_seeds.ndim == 1:
+        arr = np.ascontiguousarray(frame_seeds)
+    else:
+        arr = (np.asarray(frame_seeds, dtype=np.int64).reshape(-1) & 0xFFFFFFFF).astype(np.uint32)
+    if arr.shape[0] != n:
+        raise ValueError(f"frame_seeds has {arr.shape[0]} entries for {n} frames")
+    return arr
+
+
+def _u32ptr(arr):
+    return None if arr is None else arr.ctypes.data_as(C.POINTER(C.c_uint32))
 
 
 def stylize(prm: Params, cs: torch.Tensor, gs: torch.Tensor, lut: torch.Tensor, gt: torch.Tensor,
@@ -224,7 +239,7 @@ def stylize_batch(prm: Params, cs: torch.Tensor, gs: torch.Tensor, lut: torch.Te
     ptr = lambda t, name, dt, nd: 0 if t is None else _dev(t, name, dt, nd)  # noqa: E731
     seeds = _seeds(frame_seeds, n)
     p = prm.c()
-    check(lib().sb_stylize_batch(C.byref(p), n, seeds, cs.data_ptr(), gs.data_ptr(), ws, hs, lut.data_ptr(),
+    check(lib().sb_stylize_batch(C.byref(p), n, _u32ptr(seeds), cs.data_ptr(), gs.data_ptr(), ws, hs, lut.data_ptr(),
                                  gt.data_ptr(), wt, ht, ptr(ct, "ct", torch.uint8, (4,)),
                                  ptr(coords, "coords", torch.int32, (3,)), ptr(level, "level", torch.uint8, (3,)),
                                  _stream(stream)))
@@ -290,7 +305,7 @@ def stylize_batch_host(prm: Params, cs: torch.Tensor, gs: torch.Tensor, lut: tor
     seeds = _seeds(frame_seeds, n)
     _check_lut(prm, lut)
     p = prm.c()
-    check(lib().sb_stylize_batch_host(C.byref(p), n, seeds, _dev(cs, "cs", torch.uint8, (3,)),
+    check(lib().sb_stylize_batch_host(C.byref(p), n, _u32ptr(seeds), _dev(cs, "cs", torch.uint8, (3,)),
                                       _dev(gs, "gs", torch.uint8, (3,)), ws, hs, _dev(lut, "lut", torch.int32, (1,)),
                                       gt_host.data_ptr(), wt, ht, ct_host.data_ptr(),
                                       0 if coords_host is None else coords_host.data_ptr(),

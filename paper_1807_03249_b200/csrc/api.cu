@@ -142,8 +142,20 @@ sb_status validate(const sb_params* prm, int32_t n_frames, const uint8_t* cs, co
 sb_status launch_frames(Prepared& p, int n_frames, const uint32_t* frame_seeds, uint32_t seed_base_f0,
                         uint8_t* level, cudaStream_t st) {
     const int64_t fpx = (int64_t)p.s.wt * p.s.ht;
-    for (int f0 = 0; f0 < n_frames; f0 += sb::kSeedsPerLaunch) {
-        const int nf = (n_frames - f0) < sb::kSeedsPerLaunch ? (n_frames - f0) : sb::kSeedsPerLaunch;
+    // Seeds of the form s0 + i (the default, and the usual explicit choice) need no parameter
+    // array: the kernel derives them, and one launch covers up to 65535 frames (grid.z), so small
+    // frames fill many waves instead of a few tail-bound launches of kSeedsPerLaunch frames.
+    if (frame_seeds) {
+        bool ap = true;
+        for (int i = 1; i < n_frames && ap; ++i) ap = frame_seeds[i] == frame_seeds[0] + (uint32_t)i;
+        if (ap && n_frames > 0) {
+            seed_base_f0 = frame_seeds[0];
+            frame_seeds = nullptr;
+        }
+    }
+    const int per = frame_seeds ? sb::kSeedsPerLaunch : 65535;
+    for (int f0 = 0; f0 < n_frames; f0 += per) {
+        const int nf = (n_frames - f0) < per ? (n_frames - f0) : per;
         sb::StylizeArgs a = p.s;
         a.gt = p.s.gt + 4 * fpx * f0;
         a.ct = p.s.ct ? p.s.ct + 4 * fpx * f0 : nullptr;

@@ -436,6 +436,32 @@ def test_batch_longer_than_one_launch():
         assert (u32(co[i]) == o[1]).all() and (lv[i].cpu().numpy() == o[2]).all(), i
 
 
+def test_consecutive_seeds_one_launch_per_65535_frames():
+    """Seeds s0 + i (default or explicit) need no parameter array: the library launches up to
+    65535 frames at once (grid.z) instead of chunks of 512.  70000 tiny frames: 2 stylize
+    launches; sampled frames around the 512 and 65535 boundaries agree with the oracle."""
+    n = 70000
+    cfg = synth.CONFIGS[1]
+    cs, gs = synth.exemplar(cfg)
+    base = torch.stack([synth.heightfield_normals(8, 6, seed=9, frame=i) for i in range(5)])
+    frames = base[torch.arange(n) % 5]
+    s0 = 0xFFFFFF00  # wraps mod 2^32 inside the batch
+    seeds = [(s0 + i) & 0xFFFFFFFF for i in range(n)]
+    prm = sb.Params(threshold=cfg["t"], levels=3, guide_channels=3, seed=s0)
+    gsd = gs.to(DEV)
+    lut_d = sb.build_lut(gsd)
+    ct, co, lv = sb.stylize_batch(prm, cs.to(DEV), gsd, lut_d, frames.to(DEV), frame_seeds=seeds)
+    assert sb.launch_count() == 2
+    ct2, co2, lv2 = sb.stylize_batch(prm, cs.to(DEV), gsd, lut_d, frames.to(DEV))  # default seeds: the same
+    torch.cuda.synchronize()
+    assert torch.equal(co, co2) and torch.equal(ct, ct2) and torch.equal(lv, lv2)
+    lut = oracle_lut(gs.numpy())
+    for i in (0, 255, 511, 512, 513, 65534, 65535, 65536, n - 1):
+        o = oracle.stylize(oracle.Params(t=cfg["t"], L=3, C=3, seed=seeds[i]), cs.numpy(), gs.numpy(), lut,
+                           frames[i].numpy())
+        assert (u32(co[i]) == o[1]).all() and (lv[i].cpu().numpy() == o[2]).all(), i
+
+
 # ------------------------------------------------------------------ strided exemplar copy
 def test_prepare_exemplar_layout():
     """sb_prepare_exemplar: G_S then C_S, each hs rows of 2^16 pixels (include/styleblit.h)."""
