@@ -12,7 +12,7 @@
 //               (k1-b)^2 can never tie the total) -- the nearest occupied row above and below
 //               k1, from warp scans (one warp per column).
 //   3. resolve: one CTA per key row k1; thread k0 takes the minimum over the 256 columns of
-//               (k0-a)^2 + f(a), ties -> smaller pixel index.
+//               (k0-a)^2 + f(a), ties -> smaller pixel index (split over 4 threads per key).
 //
 // Work: ws*hs scatter + 256^2 column entries + 256^3 compare-selects (~17 M), independent of
 // the exemplar size; the 256 KB site table and the 512 KB column table stay in L2.
@@ -113,25 +113,42 @@ __global__ void __launch_bounds__(256) lut_columns_kernel(const uint32_t* __rest
     }
 }
 
-// pass 2: one CTA per key row k1; thread k0 takes the minimum over the 256 columns of
-// (k0-a)^2 + f(a), ties -> smaller pixel index.
-__global__ void __launch_bounds__(256) lut_resolve_kernel(const uint2* __restrict__ col, int ws,
-                                                          uint32_t* __restrict__ lut) {
+// pass 2: one CTA per key row k1, 1024 threads: thread (q, k0) takes the minimum over the 64
+// columns a = 64q .. 64q+63 of (k0-a)^2 + f(a), ties -> smaller pixel index; the four quarter
+// results of k0 are then combined (the (d, index) order is total, so the combination order does
+// not matter).  Four quarters instead of one thread per key: 256 CTAs on 148 SMs leave 1-2 CTAs
+// per SM, and the compare chain is latency-bound at 8 warps per SM.
+constexpr int kResolveQ = 4;
+__global__ void __launch_bounds__(256 * kResolveQ) lut_resolve_kernel(const uint2* __restrict__ col, int ws,
+                                                                      uint32_t* __restrict__ lut) {
     __shared__ uint32_t col_d[256];
     __shared__ uint32_t col_i[256];
+    __shared__ uint32_t part_d[kResolveQ][256];
+    __shared__ uint32_t part_i[kResolveQ][256];
     const int k1 = blockIdx.x;
-    const uint2 c = __ldg(col + k1 * 256 + threadIdx.x);
-    col_d[threadIdx.x] = c.x;
-    col_i[threadIdx.x] = c.y;
+    if (threadIdx.x < 256) {
+        const uint2 c = __ldg(col + k1 * 256 + threadIdx.x);
+        col_d[threadIdx.x] = c.x;
+        col_i[threadIdx.x] = c.y;
+    }
     __syncthreads();
-    const int k0 = threadIdx.x;
+    const int k0 = threadIdx.x & 255, q = threadIdx.x >> 8;
     uint32_t best_d = 0xFFFFFFFFu, best_i = 0xFFFFFFFFu;
 #pragma unroll 8
-    for (int cc = 0; cc < 256; ++cc) {
+    for (int cc = 64 * q; cc < 64 * q + 64; ++cc) {
         const uint32_t fd = col_d[cc];
         const int dx = k0 - cc;
         const uint32_t d = (fd == 0xFFFFFFFFu) ? 0xFFFFFFFFu : fd + (uint32_t)(dx * dx);
         const uint32_t fi = col_i[cc];
+        if (d < best_d || (d == best_d && fi < best_i)) { best_d = d; best_i = fi; }
+    }
+    part_d[q][k0] = best_d;
+    part_i[q][k0] = best_i;
+    __syncthreads();
+    if (q != 0) return;
+#pragma unroll
+    for (int r = 1; r < kResolveQ; ++r) {
+        const uint32_t d = part_d[r][k0], fi = part_i[r][k0];
         if (d < best_d || (d == best_d && fi < best_i)) { best_d = d; best_i = fi; }
     }
     const uint32_t y = best_i / (uint32_t)ws, x = best_i - y * (uint32_t)ws;
@@ -149,7 +166,7 @@ cudaError_t launch_build_lut(const uint8_t* gs, int ws, int hs, uint32_t* lut, v
     lut_sites_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(gs), n, site);
     uint2* col = reinterpret_cast<uint2*>(site + 65536);  // 256 x 256 (d, idx) after the sites
     lut_columns_kernel<<<32, 256, 0, st>>>(site, col);
-    lut_resolve_kernel<<<256, 256, 0, st>>>(col, ws, lut);
+    lut_resolve_kernel<<<256, 256 * kResolveQ, 0, st>>>(col, ws, lut);
     *launches += 4;
     return cudaPeekAtLastError();
 }
