@@ -222,7 +222,6 @@ __global__ void __launch_bounds__(NT, 4) vote_peel_kernel(const VoteArgs a) {
     constexpr int U = 4 + 2 * R;               // union of a block's windows: U x U positions
     constexpr int SH = TH + 2 * R;             // staged rows (tile + halo)
     constexpr int SWP = TW + 4;                // staged columns -R .. TW-1+R at so[.][R + x]
-    constexpr uint32_t NWIN = (2 * R + 1) * (2 * R + 1);
     static_assert(R >= 1 && R <= 2 && U <= 8, "peel vote: r in {1, 2}");
     __shared__ __align__(16) uint32_t so[SH][SWP];
     __shared__ __align__(16) uint32_t outc[TH][OUTW];
