@@ -41,6 +41,9 @@
 
 #include "sb_kernels.cuh"
 
+// the margin tests v >= R / v < R are trivially true / false in the R = 0 instantiations
+#pragma nv_diag_suppress 186
+
 namespace sb {
 
 namespace {
@@ -512,7 +515,7 @@ __global__ void __launch_bounds__(NT, (R <= 3 ? 6 : (R == 4 ? 5 : 4))) vote_kern
             }
         }
         // halo columns
-        for (int i = threadIdx.x; i < SH * 2 * R; i += NT) {
+        if constexpr (R > 0) for (int i = threadIdx.x; i < SH * 2 * R; i += NT) {
             const int yy = i / (2 * R), k = i - yy * (2 * R);
             const int x = k < R ? k - R : TW + (k - R);
             const int gx = x0 + x, gy = y0 - R + yy;
